@@ -416,15 +416,15 @@ static int lcp_one(int64_t n, int64_t beta, const double *bands, const double *f
         matvec_one(n, beta, bands, ue, lam);
         for (int64_t i = 0; i < n; ++i) {
             lam[i] -= f[i];
-            u[i] = ue[i] > 0.0 ? ue[i] : 0.0;   /* np.maximum(x, 0.0) */
-            if (ue[i] != ue[i]) u[i] = ue[i];   /* NaN propagates */
+            /* np.maximum(x, 0.0): (x >= 0 || isnan(x)) ? x : 0.0 (keeps -0.0) */
+            u[i] = (ue[i] >= 0.0 || ue[i] != ue[i]) ? ue[i] : 0.0;
         }
         matvec_one(n, beta, bands, u, lu);
         res = 0.0;
         for (int64_t i = 0; i < n; ++i) {
             double r = lu[i] - f[i];
-            double mn = u[i] < r ? u[i] : r;
-            if (u[i] != u[i] || r != r) mn = NAN;
+            /* np.minimum(a, b): (a <= b || isnan(a)) ? a : b (NaN propagates) */
+            double mn = (u[i] <= r || u[i] != u[i]) ? u[i] : r;
             double a = fabs(mn);
             if (a > res || a != a) res = a;
         }

@@ -1,0 +1,594 @@
+// Fused batched projected LCP -- the config-2 hot path.
+//
+// One warp owns one banded system at a time (persistent grid, static
+// striding over the batch) and runs the whole of
+// paqif_solve_lcp(LcpProblem(L, f), r=1) (paqif/parallel.py:298-347) on it:
+//
+//   active = f <= 0                                   parallel.py:312
+//   loop over passes:
+//     lmod/fmod: pinned rows keep only their diagonal  parallel.py:320-327
+//     paqif_solve(lmod, fmod, r=1):                    parallel.py:261-295
+//       factorize_wz + solve_w (fused, register windows, aqif_warp.cuh)
+//       reduced corner system (Z corner blocks, normal equations,
+//         Cholesky)                                    parallel.py:184-231
+//       solve_z(start_level = beta+1) for the middles  parallel.py:234-258
+//     lam = L u_eval - f, u = max(u_eval, 0),
+//     res = max|min(u, L u - f)|                       parallel.py:329-331
+//     return / keep best / new_active = u_eval < lam   parallel.py:332-343
+//
+// The pinned rows are never materialised: the band is streamed straight
+// from HBM and the pin is applied while loading (LcpPol::entry).  Z factor
+// records (pivot rows + W-solved right side, 38 doubles/level at beta=8) go
+// to a per-warp global stack and are read back outside-in by the Z solve
+// through a double-buffered cp.async ring in shared memory.
+#include <cfloat>
+#include "aqif_warp.cuh"
+#include "capi_util.cuh"
+
+namespace paqif {
+
+template <int BETA>
+struct LcpPol {
+  static constexpr bool kFuseW = true;
+  static constexpr bool kResidual = false;
+  using PL = PivotLayout<BETA>;
+  const double* band;
+  const uint8_t* act;
+  const double* f;
+  double* zs;
+  int n;
+  bool use_act;
+
+  __device__ __forceinline__ double raw(int i, int d) const {
+    return band[(size_t)(d + BETA) * n + i];
+  }
+  __device__ __forceinline__ bool pinned(int i) const { return use_act && act[i]; }
+  __device__ __forceinline__ double frhs(int i) const { return f[i]; }
+  __device__ __forceinline__ void on_level(int k, const double* pb, int lane) {
+    double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
+    const double2* src = reinterpret_cast<const double2*>(pb);
+    for (int idx = lane; idx < PL::kSize / 2; idx += 32) dst[idx] = src[idx];
+  }
+  __device__ __forceinline__ void on_w(int, int, double, double) {}
+  __device__ __forceinline__ void on_resid(int, int, double) {}
+};
+
+// numpy maximum(x, 0.0) / minimum(a, b) semantics (NaN propagating, -0.0 kept)
+__device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
+__device__ __forceinline__ double np_min(double a, double b) {
+  return (a <= b || a != a) ? a : b;
+}
+
+constexpr int kLcpWarpsPerBlock = 4;
+
+template <int BETA>
+struct LcpSmem {
+  using PL = PivotLayout<BETA>;
+  static constexpr int ZC = BETA * ((16 + BETA - 1) / BETA);  // chunk, multiple of BETA
+  static constexpr int kM = 2 * BETA;
+  static constexpr int kCorner = 2 * kM * kM + 2 * kM;
+  static constexpr int kRing = 2 * ZC * PL::kSize;
+  static constexpr int kScratch = kRing > kCorner ? kRing : kCorner;
+  double pbuf[2 * PL::kSize];
+  double scratch[kScratch];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Corner unknowns from the reduced system (r = 1): Rd = Z corner blocks,
+// solved through R^T R Cholesky as solve_reduced does (parallel.py:227-231).
+// Returns 0 or 1 (not SPD).
+template <int BETA, bool EXACT>
+__device__ int corner_solve(const double* zs, int n, double* x, double* cs, int lane)
+{
+  using A = Arith<EXACT>;
+  using PL = PivotLayout<BETA>;
+  constexpr int BP1 = BETA + 1, m = 2 * BETA;
+  const int s = n / 2;
+  double* rd = cs;
+  double* rtr = rd + m * m;
+  double* fd = rtr + m * m;
+  double* rtf = fd + m;
+  for (int idx = lane; idx < m * m; idx += 32) rd[idx] = 0.0;
+  __syncwarp();
+  for (int idx = lane; idx < BETA * (PL::kZ + 2); idx += 32) {
+    const int kk = idx / (PL::kZ + 2), q = idx % (PL::kZ + 2);
+    const int k = s - BETA + 1 + kk, rt = s - k, rb = n - 1 - rt;
+    const double* rec = zs + (size_t)k * PL::kSize;
+    const int brow = BETA + (rb - (n - BETA));
+    if (q < PL::kZ) {
+      const int side = q & 1, e = (q >> 1) % BP1, win = (q >> 1) / BP1;
+      const int row = side == 0 ? rt : brow;
+      if (win == 0) {
+        const int col = rt - e;
+        if (col >= 0) rd[row * m + col] = rec[q];
+      } else {
+        const int col = rb + e;
+        if (col < n) rd[row * m + BETA + (col - (n - BETA))] = rec[q];
+      }
+    } else if (q == PL::kZ) {
+      fd[rt] = rec[PL::kYT];
+    } else {
+      fd[brow] = rec[PL::kYB];
+    }
+  }
+  __syncwarp();
+  for (int idx = lane; idx < m * m; idx += 32) {
+    const int i = idx / m, j = idx % m;
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], rd[r * m + j]);
+    rtr[idx] = acc;
+  }
+  for (int i = lane; i < m; i += 32) {
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], fd[r]);
+    rtf[i] = acc;
+  }
+  __syncwarp();
+  for (int j = 0; j < m; ++j) {
+    double ajj = rtr[j * m + j];
+    for (int i = 0; i < j; ++i) ajj = A::sub(ajj, A::mul(rtr[i * m + j], rtr[i * m + j]));
+    if (!(ajj > 0.0)) return 1;
+    ajj = __dsqrt_rn(ajj);
+    __syncwarp();
+    for (int k = j + 1 + lane; k < m; k += 32) {
+      double v = rtr[j * m + k];
+      for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtr[i * m + k]));
+      rtr[j * m + k] = A::div(v, ajj);
+    }
+    if (lane == 0) rtr[j * m + j] = ajj;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int j = 0; j < m; ++j) {
+      double v = rtf[j];
+      for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtf[i]));
+      rtf[j] = A::div(v, rtr[j * m + j]);
+    }
+    for (int j = m - 1; j >= 0; --j) {
+      double v = rtf[j];
+      for (int k = j + 1; k < m; ++k) v = A::sub(v, A::mul(rtr[j * m + k], rtf[k]));
+      rtf[j] = A::div(v, rtr[j * m + j]);
+    }
+    for (int i = 0; i < BETA; ++i) {
+      x[i] = rtf[i];
+      x[n - BETA + i] = rtf[BETA + i];
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+// Middles: solve_z(start_level = BETA+1) (aqif.py:148-178, _kernels.py:175-225),
+// p = BETA .. s-1, records read outside-in through a cp.async ring.
+// Returns 0 or the 1-based breakdown level.
+template <int BETA, bool EXACT>
+__device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, int lane)
+{
+  using A = Arith<EXACT>;
+  using PL = PivotLayout<BETA>;
+  constexpr int ZC = LcpSmem<BETA>::ZC;
+  constexpr int RS = PL::kSize;
+  const int s = n / 2;
+  const int M = s - BETA;  // middle levels
+  double xl[BETA], xr[BETA];
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      xl[j] = x[j];
+      xr[j] = x[n - 1 - j];
+    }
+  }
+  auto issue = [&](int c0, int buf) {
+    const int k_hi = s - BETA - c0;
+    const int k_lo = max(1, k_hi - ZC + 1);
+    const int pieces = (k_hi - k_lo + 1) * RS / 2;
+    const double* src = zs + (size_t)k_lo * RS;
+    double* dst = ring + buf * ZC * RS;
+    for (int q = lane; q < pieces; q += 32) cp_async16(dst + 2 * q, src + 2 * q);
+    cp_async_commit();
+  };
+  int status = 0;
+  if (M > 0) issue(0, 0);
+  for (int c0 = 0, cb = 0; c0 < M; c0 += ZC, cb ^= 1) {
+    if (c0 + ZC < M) {
+      issue(c0 + ZC, cb ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    if (lane == 0 && status == 0) {
+      const int k_hi = s - BETA - c0;
+      const int k_lo = max(1, k_hi - ZC + 1);
+      const double* buf = ring + cb * ZC * RS;
+#pragma unroll
+      for (int ph = 0; ph < ZC; ++ph) {
+        const int p = BETA + c0 + ph;
+        if (p >= s) break;
+        const int q = n - 1 - p, k = s - p;
+        const double* rec = buf + (k - k_lo) * RS;
+        double rt = rec[PL::kYT], rb = rec[PL::kYB];
+#pragma unroll
+        for (int t = 0; t < BETA; ++t) {
+          const double xj = xl[(ph + t) % BETA];
+          rt = A::axpy_neg(rt, rec[PL::zi(0, BETA - t, 0)], xj);
+          rb = A::axpy_neg(rb, rec[PL::zi(0, BETA - t, 1)], xj);
+          const double xj2 = xr[(ph - 1 - t + 2 * BETA) % BETA];
+          rt = A::axpy_neg(rt, rec[PL::zi(1, 1 + t, 0)], xj2);
+          rb = A::axpy_neg(rb, rec[PL::zi(1, 1 + t, 1)], xj2);
+        }
+        const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
+        const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
+        const double det = A::det2(a11, a22, a12, a21);
+        double scale = fabs(a11);
+        if (fabs(a12) > scale) scale = fabs(a12);
+        if (fabs(a21) > scale) scale = fabs(a21);
+        if (fabs(a22) > scale) scale = fabs(a22);
+        if (fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY) {
+          status = p + 1;
+          break;
+        }
+        const double xp = A::div(A::det2(a22, rt, a12, rb), det);
+        const double xq = A::div(A::det2(a11, rb, a21, rt), det);
+        x[p] = xp;
+        x[q] = xq;
+        xl[ph % BETA] = xp;
+        xr[ph % BETA] = xq;
+      }
+    }
+    status = __shfl_sync(0xffffffffu, status, 0);
+    __syncwarp();
+    if (status) {
+      cp_async_wait<0>();
+      break;
+    }
+  }
+  __syncwarp();
+  return status;
+}
+
+template <int BETA, bool EXACT, bool SOLVE_ONLY>
+__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock)
+lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
+           double tol, int max_outer, double* u_out, uint8_t* act_out, int64_t* passes_out,
+           double* res_out, int64_t* status_out, char* ws, size_t ws_per_warp, int total_warps)
+{
+  using A = Arith<EXACT>;
+  using PL = PivotLayout<BETA>;
+  __shared__ __align__(16) LcpSmem<BETA> sm[kLcpWarpsPerBlock];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kLcpWarpsPerBlock + wid;
+  if (gw >= total_warps) return;
+  const int s = n / 2;
+  const size_t nb = (size_t)(2 * BETA + 1) * n;
+  char* my = ws + (size_t)gw * ws_per_warp;
+  double* zs = reinterpret_cast<double*>(my);
+  size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
+  double* x = reinterpret_cast<double*>(my + off);
+  off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
+  uint8_t* act = reinterpret_cast<uint8_t*>(my + off);
+  off += ((size_t)n + 255) & ~(size_t)255;
+  uint8_t* nact = reinterpret_cast<uint8_t*>(my + off);
+
+  for (int64_t b = gw; b < B; b += total_warps) {
+    const double* bd = bands + b * nb;
+    const double* fb = f + b * (size_t)n;
+    double* ub = u_out + b * (size_t)n;
+    uint8_t* ab = SOLVE_ONLY ? nullptr : act_out + b * (size_t)n;
+    double cmax = 0.0, fmax = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double fi = fb[i];
+      const uint8_t a = SOLVE_ONLY ? 0 : (fi <= 0.0);
+      act[i] = a;
+      if (!SOLVE_ONLY) {
+        ub[i] = 0.0;
+        ab[i] = a;
+        double c = 0.0;
+        for (int d = 0; d <= 2 * BETA; ++d) c = c + fabs(bd[(size_t)d * n + i]);
+        cmax = c > cmax ? c : cmax;
+        fmax = fabs(fi) > fmax ? fabs(fi) : fmax;
+      }
+    }
+    cmax = warp_max(cmax);
+    fmax = warp_max(fmax);
+    const double floor_ = 1e3 * DBL_EPSILON * (cmax + fmax);
+    const double lim = tol > floor_ ? tol : floor_;
+    double best_res = INFINITY, res = INFINITY;
+    int passes = 0, st = 0;
+    bool done = false;
+    uint8_t* cur = act;
+    uint8_t* nxt = nact;
+    for (int outer = 0; outer < max_outer; ++outer) {
+      __syncwarp();
+      LcpPol<BETA> pol;
+      pol.band = bd;
+      pol.act = cur;
+      pol.f = fb;
+      pol.zs = zs;
+      pol.n = n;
+      pol.use_act = !SOLVE_ONLY;
+      passes = outer + 1;
+      if (aqif_factor_warp<BETA, EXACT>(pol, n, 1e-14, sm[wid].pbuf, lane)) {
+        st = PAQIF_LCP_FACTOR_BREAKDOWN;
+        break;
+      }
+      __syncwarp();
+      if (corner_solve<BETA, EXACT>(zs, n, x, sm[wid].scratch, lane)) {
+        st = PAQIF_LCP_NOT_PD;
+        break;
+      }
+      if (zsolve_middle<BETA, EXACT>(zs, n, x, sm[wid].scratch, lane)) {
+        st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
+        break;
+      }
+      if (SOLVE_ONLY) {
+        for (int i = lane; i < n; i += 32) ub[i] = x[i];
+        done = true;
+        break;
+      }
+      // complementarity check and next policy (parallel.py:329-343)
+      double r = 0.0;
+      int changed = 0;
+      for (int i = lane; i < n; i += 32) {
+        double acc1 = 0.0, acc2 = 0.0;
+        const int lo = i - BETA > 0 ? i - BETA : 0;
+        const int hi = i + BETA + 1 < n ? i + BETA + 1 : n;
+        for (int j = lo; j < hi; ++j) {
+          const double a = bd[(size_t)(j - i + BETA) * n + i];
+          const double xe = x[j];
+          acc1 = A::axpy(acc1, a, xe);
+          acc2 = A::axpy(acc2, a, np_max0(xe));
+        }
+        const double xi = x[i];
+        const double lam = A::sub(acc1, fb[i]);
+        const double rr = A::sub(acc2, fb[i]);
+        const double mn = fabs(np_min(np_max0(xi), rr));
+        r = (r != r || mn != mn) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
+        const uint8_t na = xi < lam;
+        nxt[i] = na;
+        changed |= (na != cur[i]);
+      }
+      r = warp_max(r);
+      changed = __any_sync(0xffffffffu, changed);
+      res = r;
+      if (res <= tol || res < best_res) {
+        for (int i = lane; i < n; i += 32) {
+          ub[i] = np_max0(x[i]);
+          ab[i] = cur[i];
+        }
+        if (res <= tol) {
+          done = true;
+          break;
+        }
+        best_res = res;
+      }
+      if (!changed) break;
+      uint8_t* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    if (!done && st == 0) {
+      if (best_res <= lim) res = best_res;
+      else st = PAQIF_LCP_NONCONVERGED;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (passes_out) passes_out[b] = passes;
+      if (res_out) res_out[b] = res;
+      status_out[b] = st;
+    }
+  }
+}
+
+template <int BETA>
+size_t lcp_ws_per_warp(int n) {
+  using PL = PivotLayout<BETA>;
+  const int s = n / 2;
+  size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
+  off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
+  off += ((size_t)n + 255) & ~(size_t)255;
+  off += ((size_t)n + 255) & ~(size_t)255;
+  return off;
+}
+
+}  // namespace paqif
+
+using namespace paqif;
+
+namespace {
+
+template <int BETA, bool EXACT, bool SOLVE_ONLY>
+int lcp_grid_warps(int64_t B) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lcp_kernel<BETA, EXACT, SOLVE_ONLY>,
+                                                32 * kLcpWarpsPerBlock, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t w = (int64_t)sms * per_sm * kLcpWarpsPerBlock;
+  if (w > B) w = B;
+  return (int)(w < 1 ? 1 : w);
+}
+
+struct LcpDispatch {
+  int64_t B;
+  int n;
+  const double* bands;
+  const double* f;
+  double tol;
+  int max_outer;
+  double* u;
+  uint8_t* act;
+  int64_t* passes;
+  double* res;
+  int64_t* status;
+  void* ws;
+  size_t ws_bytes;
+  cudaStream_t st;
+};
+
+template <int BETA, bool EXACT, bool SOLVE_ONLY>
+int run_lcp(const LcpDispatch& a) {
+  const int warps = lcp_grid_warps<BETA, EXACT, SOLVE_ONLY>(a.B);
+  const size_t per = lcp_ws_per_warp<BETA>(a.n);
+  if (a.ws_bytes < per * (size_t)warps) {
+    std::snprintf(last_error_buf(), 512, "workspace too small: need %zu bytes",
+                  per * (size_t)warps);
+    return PAQIF_E_WORKSPACE;
+  }
+  const unsigned grid = (unsigned)((warps + kLcpWarpsPerBlock - 1) / kLcpWarpsPerBlock);
+  lcp_kernel<BETA, EXACT, SOLVE_ONLY><<<grid, 32 * kLcpWarpsPerBlock, 0, a.st>>>(
+      a.B, a.n, a.bands, a.f, a.tol, a.max_outer, a.u, a.act, a.passes, a.res, a.status,
+      (char*)a.ws, per, warps);
+  return check_launch("lcp_kernel");
+}
+
+template <bool EXACT, bool SOLVE_ONLY>
+int run_lcp_beta(int beta, const LcpDispatch& a) {
+  switch (beta) {
+    case 1: return run_lcp<1, EXACT, SOLVE_ONLY>(a);
+    case 2: return run_lcp<2, EXACT, SOLVE_ONLY>(a);
+    case 3: return run_lcp<3, EXACT, SOLVE_ONLY>(a);
+    case 4: return run_lcp<4, EXACT, SOLVE_ONLY>(a);
+    case 5: return run_lcp<5, EXACT, SOLVE_ONLY>(a);
+    case 6: return run_lcp<6, EXACT, SOLVE_ONLY>(a);
+    case 7: return run_lcp<7, EXACT, SOLVE_ONLY>(a);
+    case 8: return run_lcp<8, EXACT, SOLVE_ONLY>(a);
+    default: return set_arg_error("lcp: beta must be in 1..8");
+  }
+}
+
+size_t ws_bytes_for(int64_t B, int64_t n, int64_t beta, bool exact) {
+  size_t per = 0;
+  int warps = 1;
+  switch (beta) {
+#define PAQIF_WS_CASE(BB)                                                        \
+  case BB:                                                                       \
+    per = lcp_ws_per_warp<BB>((int)n);                                           \
+    warps = exact ? lcp_grid_warps<BB, true, false>(B) : lcp_grid_warps<BB, false, false>(B); \
+    break;
+    PAQIF_WS_CASE(1)
+    PAQIF_WS_CASE(2)
+    PAQIF_WS_CASE(3)
+    PAQIF_WS_CASE(4)
+    PAQIF_WS_CASE(5)
+    PAQIF_WS_CASE(6)
+    PAQIF_WS_CASE(7)
+    PAQIF_WS_CASE(8)
+#undef PAQIF_WS_CASE
+    default: return 0;
+  }
+  // solve-only and exact/fast variants share the layout; take the max grid
+  int w2 = 1;
+  switch (beta) {
+#define PAQIF_WS_CASE2(BB)                                                              \
+  case BB:                                                                              \
+    w2 = exact ? lcp_grid_warps<BB, true, true>(B) : lcp_grid_warps<BB, false, true>(B); \
+    break;
+    PAQIF_WS_CASE2(1)
+    PAQIF_WS_CASE2(2)
+    PAQIF_WS_CASE2(3)
+    PAQIF_WS_CASE2(4)
+    PAQIF_WS_CASE2(5)
+    PAQIF_WS_CASE2(6)
+    PAQIF_WS_CASE2(7)
+    PAQIF_WS_CASE2(8)
+#undef PAQIF_WS_CASE2
+  }
+  return per * (size_t)(warps > w2 ? warps : w2);
+}
+
+int check_lcp_args(int64_t B, int64_t n, int64_t beta) {
+  if (B < 0 || n < 2 || (n & 1)) return set_arg_error("lcp: order must be even and >= 2");
+  if (beta < 1 || beta > 8) return set_arg_error("lcp: beta must be in 1..8");
+  if (n < 2 * beta + 2) return set_arg_error("lcp: block size must exceed 2*beta (PartitionError)");
+  if (n > (1 << 26)) return set_arg_error("lcp: order too large");
+  return PAQIF_OK;
+}
+
+}  // namespace
+
+extern "C" size_t paqif_lcp_workspace_bytes(int64_t B, int64_t n, int64_t beta) {
+  if (check_lcp_args(B, n, beta) || B == 0) return 0;
+  const size_t a = ws_bytes_for(B, n, beta, true), b = ws_bytes_for(B, n, beta, false);
+  return a > b ? a : b;
+}
+
+extern "C" int paqif_lcp_batch(int64_t B, int64_t n, int64_t beta, const double* bands,
+                               const double* f, double tol, int64_t max_outer, uint32_t flags,
+                               double* u, uint8_t* active, int64_t* passes, double* res,
+                               int64_t* status, void* workspace, size_t workspace_bytes,
+                               void* stream)
+{
+  if (int rc = check_lcp_args(B, n, beta)) return rc;
+  if (B == 0) return PAQIF_OK;
+  if (max_outer < 0 || max_outer > (1 << 30)) return set_arg_error("lcp: max_outer");
+  LcpDispatch a{B, (int)n, bands, f, tol, (int)max_outer, u, active, passes, res, status,
+                workspace, workspace_bytes, (cudaStream_t)stream};
+  if (flags & PAQIF_FLAG_EXACT) return run_lcp_beta<true, false>((int)beta, a);
+  return run_lcp_beta<false, false>((int)beta, a);
+}
+
+extern "C" int paqif_solve_r1_batch(int64_t B, int64_t n, int64_t beta, const double* bands,
+                                    const double* f, double* x, int64_t* status, uint32_t flags,
+                                    void* workspace, size_t workspace_bytes, void* stream)
+{
+  if (int rc = check_lcp_args(B, n, beta)) return rc;
+  if (B == 0) return PAQIF_OK;
+  LcpDispatch a{B, (int)n, bands, f, 0.0, 1, x, nullptr, nullptr, nullptr, status,
+                workspace, workspace_bytes, (cudaStream_t)stream};
+  if (flags & PAQIF_FLAG_EXACT) return run_lcp_beta<true, true>((int)beta, a);
+  return run_lcp_beta<false, true>((int)beta, a);
+}
+
+extern "C" int paqif_lcp_batch_host(int64_t B, int64_t n, int64_t beta, const double* bands,
+                                    const double* f, double tol, int64_t max_outer,
+                                    uint32_t flags, double* u, uint8_t* active, int64_t* passes,
+                                    double* res, int64_t* status)
+{
+  if (int rc = check_lcp_args(B, n, beta)) return rc;
+  if (B == 0) return PAQIF_OK;
+  const size_t nb = (size_t)B * (2 * beta + 1) * n, nv = (size_t)B * n;
+  const size_t wsb = paqif_lcp_workspace_bytes(B, n, beta);
+  DevBuf<double> d_b(nb), d_f(nv), d_u(nv), d_r(B);
+  DevBuf<uint8_t> d_a(nv);
+  DevBuf<int64_t> d_p(B), d_s(B);
+  DevBuf<char> d_ws(wsb);
+  if (!d_b.ok() || !d_f.ok() || !d_u.ok() || !d_r.ok() || !d_a.ok() || !d_p.ok() || !d_s.ok() ||
+      !d_ws.ok())
+    return set_cuda_error("lcp_host: alloc", cudaErrorMemoryAllocation);
+  cudaStream_t st;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return set_cuda_error("lcp_host: stream", e);
+  int rc = PAQIF_OK;
+  if ((e = cudaMemcpyAsync(d_b.p, bands, nb * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_f.p, f, nv * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+    rc = set_cuda_error("lcp_host: h2d", e);
+  }
+  if (!rc)
+    rc = paqif_lcp_batch(B, n, beta, d_b.p, d_f.p, tol, max_outer, flags, d_u.p, d_a.p, d_p.p,
+                         d_r.p, d_s.p, d_ws.p, wsb, st);
+  if (!rc) {
+    if ((e = cudaMemcpyAsync(u, d_u.p, nv * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(active, d_a.p, nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(passes, d_p.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(res, d_r.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(status, d_s.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      rc = set_cuda_error("lcp_host: d2h", e);
+  }
+  e = cudaStreamSynchronize(st);
+  if (!rc && e != cudaSuccess) rc = set_cuda_error("lcp_host: sync", e);
+  cudaStreamDestroy(st);
+  return rc;
+}
