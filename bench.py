@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark: batched PAQIF banded-LCP solve (BASELINE.json configs[1]).
+
+Workload (per GPU, weak scaling): 4096 independent banded LCPs, n = 1025
+(padded to 1026 with a pinned identity row), semibandwidth 8, seeded
+synthetic inputs (paper_2008_03276_b200/workloads.py).  One "step" = one
+fused-kernel launch that runs the reference's whole projected active-set
+solve paqif_solve_lcp(r=1) on every system of the batch (2-4 factor + W + Z
+passes each).  Rank r solves systems [4096 r, 4096 (r+1)) -- no collective on
+the data path; NCCL only carries the max-over-ranks timing.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--fast]
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks; inputs (571 MB of bands
+per GPU) exceed the 126 MB L2, so no explicit flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS = 1025          # unpadded order of one LCP (rows solved)
+N_PAD = 1026
+BETA = 8
+B_PER_GPU = 4096
+SEED = 2024
+# algorithmic bytes per LCP: band (2beta+1)*n + f + u, float64
+BYTES_PER_LCP = ((2 * BETA + 1) * N_ROWS + N_ROWS + N_ROWS) * 8
+METRIC = "PAQIF banded-LCP rows solved/s"
+UNIT = "rows/s"
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6551.4, "src": "fallback"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        peaks["hbm_gbs"] = float(d.get("hbm_gbs", peaks["hbm_gbs"]))
+        peaks["src"] = "MEASURED_PEAKS.json"
+    peaks["fp64_tflops"] = 33.94  # DFMA microbenchmark, profiles/peaks_r01.json
+    p2 = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    if os.path.exists(p2):
+        with open(p2) as fh:
+            peaks["fp64_tflops"] = float(json.load(fh)["dfma_tflops"])
+    return peaks
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the LCP kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "lcp_ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get("dram_bytes_per_launch"), d.get("systems_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the
+    timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            lines = [l.strip() for l in open(self.path) if l.strip()]
+        except OSError:
+            return out
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if sm:
+            out["sm_mhz"] = statistics.median(sm)
+            out["sm_max_mhz"] = mx
+            out["samples"] = len(sm)
+        out["reasons"] = sorted(reasons)
+        return out
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_rate(bands, f, threads: int, min_core_seconds: float = 10.0):
+    """The reference algorithm's CPU path (the C oracle port of
+    paqif_solve_lcp(r=1), oracle/paqif_oracle.c) on the given config-2
+    systems with `threads` host threads, repeated until at least
+    `min_core_seconds` of CPU work.  Returns (rows/s, wall s, reps)."""
+    import oracle
+    reps, wall = 0, 0.0
+    while reps == 0 or wall * threads < min_core_seconds:
+        t0 = time.perf_counter()
+        oracle.lcp_batch(bands, f, threads=threads)
+        wall += time.perf_counter() - t0
+        reps += 1
+    return reps * bands.shape[0] * N_ROWS / wall, wall, reps
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path
+    (oracle port, all host threads), rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2008_03276_b200.workloads import lcp_batch
+    threads = cpu_threads()
+    sample = B_PER_GPU  # one step = the same 4096-system batch the GPU step solves
+    bands, f = lcp_batch(SEED, sample)
+    for _ in range(args.warmup):
+        oracle.lcp_batch(bands[:64], f[:64], threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.lcp_batch(bands, f, threads=threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = sample * N_ROWS / (sum(times) / len(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, workloads.lcp_batch)",
+        "config": {"workload": "config2: banded LCP batch, n=1025 (pad 1026), beta=8",
+                   "systems_per_step": sample, "seed": SEED},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} config-2 systems per step (oracle/paqif_oracle.c "
+                                   f"restating paqif_solve_lcp r=1), {threads} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--fast", action="store_true", help="FMA arithmetic (default: exact)")
+    ap.add_argument("--batch", type=int, default=B_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2008_03276_b200 import _native
+    from paper_2008_03276_b200.batch import LcpSolver
+    from paper_2008_03276_b200.workloads import lcp_batch
+
+    B = args.batch
+    exact = not args.fast
+    bands_h, f_h = lcp_batch(SEED, B, start=rank * B)
+    # pinned host copies: the e2e path reads these every step
+    bands_pin = torch.from_numpy(bands_h).pin_memory()
+    f_pin = torch.from_numpy(f_h).pin_memory()
+    bands = bands_pin.to("cuda", non_blocking=True)
+    f = f_pin.to("cuda", non_blocking=True)
+    solver = LcpSolver(B, N_PAD, BETA, exact)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        solver.launch(bands, f)
+    barrier()
+    with ClockSampler(local) as clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            solver.launch(bands, f)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    status = solver.status.cpu().numpy()
+    passes = solver.passes.cpu().numpy()
+    if np.any(status != 0):
+        raise SystemExit(f"LCP status != 0 on {int(np.sum(status != 0))} systems")
+    value = world * B * N_ROWS / (ms_step * 1e-3)
+
+    # ---- end to end through the C-ABI host entry (pinned host buffers in/out)
+    L = _native.lib()
+    u_h = torch.empty((B, N_PAD), dtype=torch.float64).pin_memory()
+    a_h = torch.empty((B, N_PAD), dtype=torch.uint8).pin_memory()
+    p_h = torch.empty(B, dtype=torch.int64).pin_memory()
+    r_h = torch.empty(B, dtype=torch.float64).pin_memory()
+    s_h = torch.empty(B, dtype=torch.int64).pin_memory()
+
+    def host_call():
+        rc = L.paqif_lcp_batch_host(B, N_PAD, BETA, bands_pin.data_ptr(), f_pin.data_ptr(),
+                                    1e-10, 100, _native.FLAG_EXACT if exact else 0,
+                                    u_h.data_ptr(), a_h.data_ptr(), p_h.data_ptr(),
+                                    r_h.data_ptr(), s_h.data_ptr())
+        _native.check(rc, "paqif_lcp_batch_host")
+
+    host_call()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        host_call()
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_value = world * B * N_ROWS / e2e_s
+    if not np.array_equal(u_h.numpy(), solver.u.cpu().numpy()):
+        raise SystemExit("host-entry result differs from device-entry result")
+    h2d = bands_h.nbytes + f_h.nbytes
+    d2h = u_h.numel() * 8 + a_h.numel() + 3 * B * 8
+
+    # ---- roofline of the dominant (only) kernel
+    peaks = load_peaks()
+    achieved_gbs = B * BYTES_PER_LCP / (ms_step * 1e-3) / 1e9
+    traffic, traffic_b = ncu_traffic()
+    if traffic is not None and traffic_b:
+        traffic = traffic * B / traffic_b
+    from paper_2008_03276_b200.parallel import CostModel
+    flops_pass = CostModel(N_PAD, BETA, 1).serial_total()  # paper's op count, one pass
+    fp64_tflops = B * float(np.mean(passes)) * flops_pass / (ms_step * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded per system, workloads.lcp_batch; inputs 571 MB/GPU > L2, "
+                "no flush needed)",
+        "config": {"workload": "config2: 4096 banded LCPs/GPU, n=1025 (pad 1026), beta=8, "
+                               "paqif_solve_lcp(r=1) semantics",
+                   "systems_per_gpu": B, "n": N_ROWS, "beta": BETA, "seed": SEED,
+                   "arith": "exact (reference rounding, bit-exact vs oracle)" if exact
+                   else "fma", "mean_passes": float(np.mean(passes)),
+                   "l2": "inputs larger than L2"},
+        "gpu_launches": args.steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "path": "C ABI paqif_lcp_batch_host, pinned host buffers"},
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved_gbs / peaks["hbm_gbs"],
+                     "traffic": traffic,
+                     "peak_src": peaks["src"],
+                     "algorithmic_bytes_per_launch": B * BYTES_PER_LCP},
+        "fp64": {"achieved_tflops": fp64_tflops, "peak_tflops": peaks["fp64_tflops"],
+                 "frac": fp64_tflops / peaks["fp64_tflops"],
+                 "count": "CostModel(1026,8,1).serial_total() per pass x mean passes",
+                 "peak_src": "tools/peaks.cu DFMA microbenchmark (profiles/peaks_r01.json)"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        sample = 1024
+        rate, secs, reps = cpu_reference_rate(bands_h[:sample], f_h[:sample], threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"first {sample} systems of the GPU batch x {reps}, "
+                                          f"oracle/paqif_oracle.c (C restatement of "
+                                          f"paqif_solve_lcp r=1), {secs:.1f} s wall"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

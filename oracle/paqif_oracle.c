@@ -254,6 +254,10 @@ typedef struct {
     double *band, *anti, *z2x2, *zl, *zr, *ww, *y, *x;
     double *rd, *rtr, *rtf;
     int64_t *trace;
+    /* LCP driver buffers (allocated once per worker: per-call malloc of
+       >128 KB goes through mmap and serialises threads on page faults) */
+    double *lmod, *fmod, *ue, *lam, *u, *lu, *best_u;
+    uint8_t *active, *nact, *best_act;
 } work_t;
 
 static void work_alloc(work_t *w, int64_t n, int64_t beta)
@@ -271,12 +275,24 @@ static void work_alloc(work_t *w, int64_t n, int64_t beta)
     w->rtr = malloc(sizeof(double) * m * m);
     w->rtf = malloc(sizeof(double) * m);
     w->trace = NULL;
+    w->lmod = malloc(sizeof(double) * nb);
+    w->fmod = malloc(sizeof(double) * n);
+    w->ue = malloc(sizeof(double) * n);
+    w->lam = malloc(sizeof(double) * n);
+    w->u = malloc(sizeof(double) * n);
+    w->lu = malloc(sizeof(double) * n);
+    w->best_u = malloc(sizeof(double) * n);
+    w->active = malloc(n);
+    w->nact = malloc(n);
+    w->best_act = malloc(n);
 }
 
 static void work_free(work_t *w)
 {
     free(w->band); free(w->anti); free(w->z2x2); free(w->zl); free(w->zr); free(w->ww);
     free(w->y); free(w->x); free(w->rd); free(w->rtr); free(w->rtf);
+    free(w->lmod); free(w->fmod); free(w->ue); free(w->lam); free(w->u); free(w->lu);
+    free(w->best_u); free(w->active); free(w->nact); free(w->best_act);
 }
 
 /* Cholesky of the SPD normal matrix (upper, A = U^T U) + two triangular
@@ -379,11 +395,10 @@ static int lcp_one(int64_t n, int64_t beta, const double *bands, const double *f
                    int64_t *passes_out, double *res_out, work_t *w)
 {
     const int64_t nb = (2 * beta + 1) * n;
-    double *lmod = malloc(sizeof(double) * nb), *fmod = malloc(sizeof(double) * n);
-    double *ue = malloc(sizeof(double) * n), *lam = malloc(sizeof(double) * n);
-    double *u = malloc(sizeof(double) * n), *lu = malloc(sizeof(double) * n);
-    double *best_u = calloc(n, sizeof(double));
-    uint8_t *active = malloc(n), *nact = malloc(n), *best_act = malloc(n);
+    double *lmod = w->lmod, *fmod = w->fmod, *ue = w->ue, *lam = w->lam, *u = w->u, *lu = w->lu;
+    double *best_u = w->best_u;
+    uint8_t *active = w->active, *nact = w->nact, *best_act = w->best_act;
+    memset(best_u, 0, sizeof(double) * n);
     int rc = OR_NONCONVERGED;
     int64_t passes = 0;
     double res = INFINITY, best_res = INFINITY;
@@ -457,8 +472,6 @@ static int lcp_one(int64_t n, int64_t beta, const double *bands, const double *f
 done:
     *passes_out = passes;
     *res_out = res;
-    free(lmod); free(fmod); free(ue); free(lam); free(u); free(lu); free(best_u);
-    free(active); free(nact); free(best_act);
     return rc;
 }
 

@@ -22,6 +22,7 @@
 // to a per-warp global stack and are read back outside-in by the Z solve
 // through a double-buffered cp.async ring in shared memory.
 #include <cfloat>
+#include <mutex>
 #include "aqif_warp.cuh"
 #include "capi_util.cuh"
 
@@ -552,6 +553,43 @@ extern "C" int paqif_solve_r1_batch(int64_t B, int64_t n, int64_t beta, const do
   return run_lcp_beta<false, true>((int)beta, a);
 }
 
+namespace {
+// Device staging reused across host-entry calls (grown on demand), so the
+// host path pays for copies and the kernel, not for cudaMalloc each call.
+struct HostStage {
+  std::mutex mu;
+  char* buf = nullptr;
+  size_t cap = 0;
+  cudaStream_t st = nullptr;
+  int device = -1;
+  char* get(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != device) {
+      // a different device: the old allocation belongs to another context
+      buf = nullptr;
+      cap = 0;
+      st = nullptr;
+      device = dev;
+    }
+    if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (bytes > cap) {
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      cap = 0;
+      if (cudaMalloc(&buf, bytes) != cudaSuccess) return nullptr;
+      cap = bytes;
+    }
+    return buf;
+  }
+};
+HostStage& host_stage() {
+  static HostStage h;
+  return h;
+}
+size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+}  // namespace
+
 extern "C" int paqif_lcp_batch_host(int64_t B, int64_t n, int64_t beta, const double* bands,
                                     const double* f, double tol, int64_t max_outer,
                                     uint32_t flags, double* u, uint8_t* active, int64_t* passes,
@@ -561,34 +599,38 @@ extern "C" int paqif_lcp_batch_host(int64_t B, int64_t n, int64_t beta, const do
   if (B == 0) return PAQIF_OK;
   const size_t nb = (size_t)B * (2 * beta + 1) * n, nv = (size_t)B * n;
   const size_t wsb = paqif_lcp_workspace_bytes(B, n, beta);
-  DevBuf<double> d_b(nb), d_f(nv), d_u(nv), d_r(B);
-  DevBuf<uint8_t> d_a(nv);
-  DevBuf<int64_t> d_p(B), d_s(B);
-  DevBuf<char> d_ws(wsb);
-  if (!d_b.ok() || !d_f.ok() || !d_u.ok() || !d_r.ok() || !d_a.ok() || !d_p.ok() || !d_s.ok() ||
-      !d_ws.ok())
-    return set_cuda_error("lcp_host: alloc", cudaErrorMemoryAllocation);
-  cudaStream_t st;
-  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  if (e != cudaSuccess) return set_cuda_error("lcp_host: stream", e);
+  const size_t o_b = 0, o_f = o_b + al256(nb * 8), o_u = o_f + al256(nv * 8),
+               o_a = o_u + al256(nv * 8), o_p = o_a + al256(nv), o_r = o_p + al256(B * 8),
+               o_s = o_r + al256(B * 8), o_w = o_s + al256(B * 8), total = o_w + al256(wsb);
+  HostStage& hs = host_stage();
+  std::lock_guard<std::mutex> lock(hs.mu);
+  char* base = hs.get(total);
+  if (!base) return set_cuda_error("lcp_host: device staging", cudaErrorMemoryAllocation);
+  cudaStream_t st = hs.st;
+  double* d_b = (double*)(base + o_b);
+  double* d_f = (double*)(base + o_f);
+  double* d_u = (double*)(base + o_u);
+  uint8_t* d_a = (uint8_t*)(base + o_a);
+  int64_t* d_p = (int64_t*)(base + o_p);
+  double* d_r = (double*)(base + o_r);
+  int64_t* d_s = (int64_t*)(base + o_s);
   int rc = PAQIF_OK;
-  if ((e = cudaMemcpyAsync(d_b.p, bands, nb * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d_f.p, f, nv * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(d_b, bands, nb * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_f, f, nv * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     rc = set_cuda_error("lcp_host: h2d", e);
-  }
   if (!rc)
-    rc = paqif_lcp_batch(B, n, beta, d_b.p, d_f.p, tol, max_outer, flags, d_u.p, d_a.p, d_p.p,
-                         d_r.p, d_s.p, d_ws.p, wsb, st);
+    rc = paqif_lcp_batch(B, n, beta, d_b, d_f, tol, max_outer, flags, d_u, d_a, d_p, d_r, d_s,
+                         base + o_w, wsb, st);
   if (!rc) {
-    if ((e = cudaMemcpyAsync(u, d_u.p, nv * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(active, d_a.p, nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(passes, d_p.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(res, d_r.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(status, d_s.p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(u, d_u, nv * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(active, d_a, nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(passes, d_p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(res, d_r, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(status, d_s, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
       rc = set_cuda_error("lcp_host: d2h", e);
   }
   e = cudaStreamSynchronize(st);
   if (!rc && e != cudaSuccess) rc = set_cuda_error("lcp_host: sync", e);
-  cudaStreamDestroy(st);
   return rc;
 }
