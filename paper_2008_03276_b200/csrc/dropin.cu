@@ -21,6 +21,7 @@ template <int BETA>
 struct DropinPol {
   static constexpr bool kFuseW = false;
   static constexpr bool kResidual = true;
+  static constexpr bool kRecordW = true;
   static constexpr int BP1 = BETA + 1;
   double* band;
   double* anti;
@@ -30,15 +31,18 @@ struct DropinPol {
   double* ww;
   int n;
 
-  __device__ __forceinline__ double raw(int i, int d) const {
-    return band[(size_t)(d + BETA) * n + i];
+  __device__ __forceinline__ const double* raw_ptr(int i, int d) const {
+    return band + (size_t)(d + BETA) * n + i;
   }
+  __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
+  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
   __device__ __forceinline__ bool pinned(int) const { return false; }
+  __device__ __forceinline__ const double* frhs_ptr(int) const { return nullptr; }
   __device__ __forceinline__ double frhs(int) const { return 0.0; }
-  __device__ __forceinline__ void on_level(int k, const double* pb, int lane) {
+  __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
     using PL = PivotLayout<BETA>;
     const int s = n / 2, rt = s - k, rb = s + k - 1;
-    for (int idx = lane; idx < PL::kZ; idx += 32) {
+    for (int idx = gl; idx < PL::kZ; idx += G) {
       const int side = idx & 1, e = (idx >> 1) % BP1, win = (idx >> 1) / BP1;
       const double v = pb[idx];
       if (win == 0) {
@@ -47,7 +51,7 @@ struct DropinPol {
         if (rb + e < n) zr[((size_t)k * 2 + side) * BP1 + e] = v;
       }
     }
-    if (lane == 0) {
+    if (gl == 0) {
       double* z = z2x2 + (size_t)k * 4;
       z[0] = pb[PL::zi(0, 0, 0)];
       z[1] = pb[PL::zi(1, 0, 0)];
@@ -78,23 +82,28 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 factor_warp_kernel(int64_t B, int n, double* band, double* anti, double* z2x2, double* zl,
                    double* zr, double* ww, double tol, int64_t* status)
 {
-  using PL = PivotLayout<BETA>;
-  __shared__ __align__(16) double pbuf[kWarpsPerBlock][2 * PL::kSize];
+  constexpr int G = Group<BETA>::G, P = Group<BETA>::P;
+  extern __shared__ __align__(16) unsigned char dropin_dyn_smem[];
+  EngineSmem<BETA>* sm = reinterpret_cast<EngineSmem<BETA>*>(dropin_dyn_smem);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * kWarpsPerBlock + wid;
-  if (b >= B) return;
+  const int g = lane / G, gl = lane % G;
+  const int64_t wb = ((int64_t)blockIdx.x * kWarpsPerBlock + wid) * P;
+  if (wb >= B) return;  // whole warp past the batch
+  const int64_t b = wb + g;
+  const bool have = b < B;
+  const int64_t bb = have ? b : wb;
   const int s = n / 2;
   const size_t nb = (size_t)(2 * BETA + 1) * n;
   DropinPol<BETA> pol;
-  pol.band = band + b * nb;
-  pol.anti = anti + b * nb;
-  pol.z2x2 = z2x2 + b * (size_t)(s + 1) * 4;
-  pol.zl = zl + b * (size_t)(s + 1) * 2 * (BETA + 1);
-  pol.zr = zr + b * (size_t)(s + 1) * 2 * (BETA + 1);
-  pol.ww = ww + b * (size_t)(s + 1) * 4 * BETA;
+  pol.band = band + bb * nb;
+  pol.anti = anti + bb * nb;
+  pol.z2x2 = z2x2 + bb * (size_t)(s + 1) * 4;
+  pol.zl = zl + bb * (size_t)(s + 1) * 2 * (BETA + 1);
+  pol.zr = zr + bb * (size_t)(s + 1) * 2 * (BETA + 1);
+  pol.ww = ww + bb * (size_t)(s + 1) * 4 * BETA;
   pol.n = n;
-  const int st = aqif_factor_warp<BETA, EXACT>(pol, n, tol, pbuf[wid], lane);
-  if (lane == 0) status[b] = st;
+  const int st = aqif_factor_group<BETA, EXACT>(pol, n, tol, sm[wid * P + g], gl, have);
+  if (have && gl == 0) status[b] = st;
 }
 
 // Generic beta: direct restatement on the cross layout, one thread per system.
@@ -334,13 +343,18 @@ static void launch_factor(int64_t B, int n, int beta, double* band, double* anti
                           double* zl, double* zr, double* ww, double tol, int64_t* status,
                           cudaStream_t st)
 {
-  const unsigned grid = (unsigned)((B + kWarpsPerBlock - 1) / kWarpsPerBlock);
   const unsigned blk = 32 * kWarpsPerBlock;
-#define PAQIF_FACTOR_CASE(BB)                                                                \
-  case BB:                                                                                   \
-    factor_warp_kernel<BB, EXACT><<<grid, blk, 0, st>>>(B, n, band, anti, z2x2, zl, zr, ww, \
-                                                        tol, status);                        \
-    break;
+#define PAQIF_FACTOR_CASE(BB)                                                                 \
+  case BB: {                                                                                  \
+    const int64_t per_block = (int64_t)kWarpsPerBlock * Group<BB>::P;                          \
+    const unsigned grid = (unsigned)((B + per_block - 1) / per_block);                         \
+    const size_t smem = sizeof(EngineSmem<BB>) * per_block;                                    \
+    cudaFuncSetAttribute(factor_warp_kernel<BB, EXACT>,                                        \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    factor_warp_kernel<BB, EXACT><<<grid, blk, smem, st>>>(B, n, band, anti, z2x2, zl, zr, ww, \
+                                                           tol, status);                      \
+    break;                                                                                    \
+  }
   switch (beta) {
     PAQIF_FACTOR_CASE(1)
     PAQIF_FACTOR_CASE(2)

@@ -32,27 +32,35 @@ template <int BETA>
 struct LcpPol {
   static constexpr bool kFuseW = true;
   static constexpr bool kResidual = false;
+  static constexpr bool kRecordW = false;
   using PL = PivotLayout<BETA>;
   const double* band;
-  const uint8_t* act;
+  const uint32_t* act;
   const double* f;
   double* zs;
   int n;
   bool use_act;
 
-  __device__ __forceinline__ double raw(int i, int d) const {
-    return band[(size_t)(d + BETA) * n + i];
+  __device__ __forceinline__ const double* raw_ptr(int i, int d) const {
+    return band + (size_t)(d + BETA) * n + i;
   }
-  __device__ __forceinline__ bool pinned(int i) const { return use_act && act[i]; }
+  __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
+  __device__ __forceinline__ const uint32_t* pin_ptr(int i) const {
+    return use_act ? act + i : nullptr;
+  }
+  __device__ __forceinline__ bool pinned(int i) const { return use_act && act[i] != 0u; }
+  __device__ __forceinline__ const double* frhs_ptr(int i) const { return f + i; }
   __device__ __forceinline__ double frhs(int i) const { return f[i]; }
-  __device__ __forceinline__ void on_level(int k, const double* pb, int lane) {
+  __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
     double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
     const double2* src = reinterpret_cast<const double2*>(pb);
-    for (int idx = lane; idx < PL::kSize / 2; idx += 32) dst[idx] = src[idx];
+    for (int idx = gl; idx < PL::kSize / 2; idx += G) dst[idx] = src[idx];
   }
   __device__ __forceinline__ void on_w(int, int, double, double) {}
   __device__ __forceinline__ void on_resid(int, int, double) {}
 };
+
+__device__ __forceinline__ double fmax_(double a, double b) { return b > a ? b : a; }
 
 // numpy maximum(x, 0.0) / minimum(a, b) semantics (NaN propagating, -0.0 kept)
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
@@ -62,95 +70,115 @@ __device__ __forceinline__ double np_min(double a, double b) {
 
 constexpr int kLcpWarpsPerBlock = 4;
 
+#ifdef PAQIF_PROFILE_PHASES
+// dev-only phase timers (tools/phase_prof.cu): factor, corner, zsolve, check
+__device__ unsigned long long g_phase_cycles[4];
+#define PAQIF_TSTAMP(v) const long long v = clock64()
+#define PAQIF_TACC(i, a, b) ph_acc[i] += (unsigned long long)((b) - (a))
+#else
+#define PAQIF_TSTAMP(v)
+#define PAQIF_TACC(i, a, b)
+#endif
+
 template <int BETA>
 struct LcpSmem {
   using PL = PivotLayout<BETA>;
-  static constexpr int ZC = BETA * ((16 + BETA - 1) / BETA);  // chunk, multiple of BETA
+  static constexpr int ZC = BETA * ((8 + BETA - 1) / BETA);  // chunk, multiple of BETA
   static constexpr int kM = 2 * BETA;
   static constexpr int kCorner = 2 * kM * kM + 2 * kM;
   static constexpr int kRing = 2 * ZC * PL::kSize;
   static constexpr int kScratch = kRing > kCorner ? kRing : kCorner;
-  double pbuf[2 * PL::kSize];
-  double scratch[kScratch];
+  // the factorization's prefetch slots and the Z-solve ring / corner system
+  // are live in different phases and share storage
+  union {
+    EngineSmem<BETA> eng;
+    struct {
+      double pbuf_[2 * PL::kSize];
+      double scratch[kScratch];
+    } post;
+  };
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // Corner unknowns from the reduced system (r = 1): Rd = Z corner blocks,
 // solved through R^T R Cholesky as solve_reduced does (parallel.py:227-231).
+// Runs on the G lanes of the system's group; all 32 lanes call (syncs).
 // Returns 0 or 1 (not SPD).
 template <int BETA, bool EXACT>
-__device__ int corner_solve(const double* zs, int n, double* x, double* cs, int lane)
+__device__ int corner_solve(const double* zs, int n, double* x, double* cs, int gl, bool alive)
 {
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
   constexpr int BP1 = BETA + 1, m = 2 * BETA;
+  constexpr int G = Group<BETA>::G;
   const int s = n / 2;
   double* rd = cs;
   double* rtr = rd + m * m;
   double* fd = rtr + m * m;
   double* rtf = fd + m;
-  for (int idx = lane; idx < m * m; idx += 32) rd[idx] = 0.0;
+  if (alive)
+    for (int idx = gl; idx < m * m; idx += G) rd[idx] = 0.0;
   __syncwarp();
-  for (int idx = lane; idx < BETA * (PL::kZ + 2); idx += 32) {
-    const int kk = idx / (PL::kZ + 2), q = idx % (PL::kZ + 2);
-    const int k = s - BETA + 1 + kk, rt = s - k, rb = n - 1 - rt;
-    const double* rec = zs + (size_t)k * PL::kSize;
-    const int brow = BETA + (rb - (n - BETA));
-    if (q < PL::kZ) {
-      const int side = q & 1, e = (q >> 1) % BP1, win = (q >> 1) / BP1;
-      const int row = side == 0 ? rt : brow;
-      if (win == 0) {
-        const int col = rt - e;
-        if (col >= 0) rd[row * m + col] = rec[q];
+  if (alive) {
+    for (int idx = gl; idx < BETA * (PL::kZ + 2); idx += G) {
+      const int kk = idx / (PL::kZ + 2), q = idx % (PL::kZ + 2);
+      const int k = s - BETA + 1 + kk, rt = s - k, rb = n - 1 - rt;
+      const double* rec = zs + (size_t)k * PL::kSize;
+      const int brow = BETA + (rb - (n - BETA));
+      if (q < PL::kZ) {
+        const int side = q & 1, e = (q >> 1) % BP1, win = (q >> 1) / BP1;
+        const int row = side == 0 ? rt : brow;
+        if (win == 0) {
+          const int col = rt - e;
+          if (col >= 0) rd[row * m + col] = rec[q];
+        } else {
+          const int col = rb + e;
+          if (col < n) rd[row * m + BETA + (col - (n - BETA))] = rec[q];
+        }
+      } else if (q == PL::kZ) {
+        fd[rt] = rec[PL::kYT];
       } else {
-        const int col = rb + e;
-        if (col < n) rd[row * m + BETA + (col - (n - BETA))] = rec[q];
+        fd[brow] = rec[PL::kYB];
       }
-    } else if (q == PL::kZ) {
-      fd[rt] = rec[PL::kYT];
-    } else {
-      fd[brow] = rec[PL::kYB];
     }
   }
   __syncwarp();
-  for (int idx = lane; idx < m * m; idx += 32) {
-    const int i = idx / m, j = idx % m;
-    double acc = 0.0;
+  if (alive) {
+    for (int idx = gl; idx < m * m; idx += G) {
+      const int i = idx / m, j = idx % m;
+      double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], rd[r * m + j]);
-    rtr[idx] = acc;
-  }
-  for (int i = lane; i < m; i += 32) {
-    double acc = 0.0;
+      for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], rd[r * m + j]);
+      rtr[idx] = acc;
+    }
+    for (int i = gl; i < m; i += G) {
+      double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], fd[r]);
-    rtf[i] = acc;
+      for (int r = 0; r < m; ++r) acc = A::axpy(acc, rd[r * m + i], fd[r]);
+      rtf[i] = acc;
+    }
   }
   __syncwarp();
+  int fail = 0;
   for (int j = 0; j < m; ++j) {
-    double ajj = rtr[j * m + j];
-    for (int i = 0; i < j; ++i) ajj = A::sub(ajj, A::mul(rtr[i * m + j], rtr[i * m + j]));
-    if (!(ajj > 0.0)) return 1;
-    ajj = __dsqrt_rn(ajj);
-    __syncwarp();
-    for (int k = j + 1 + lane; k < m; k += 32) {
-      double v = rtr[j * m + k];
-      for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtr[i * m + k]));
-      rtr[j * m + k] = A::div(v, ajj);
+    double ajj = 0.0;
+    if (alive && !fail) {
+      ajj = rtr[j * m + j];
+      for (int i = 0; i < j; ++i) ajj = A::sub(ajj, A::mul(rtr[i * m + j], rtr[i * m + j]));
+      if (!(ajj > 0.0)) fail = 1;
+      ajj = __dsqrt_rn(ajj);
     }
-    if (lane == 0) rtr[j * m + j] = ajj;
+    __syncwarp();
+    if (alive && !fail) {
+      for (int k = j + 1 + gl; k < m; k += G) {
+        double v = rtr[j * m + k];
+        for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtr[i * m + k]));
+        rtr[j * m + k] = A::div(v, ajj);
+      }
+      if (gl == 0) rtr[j * m + j] = ajj;
+    }
     __syncwarp();
   }
-  if (lane == 0) {
+  if (alive && !fail && gl == 0) {
     for (int j = 0; j < m; ++j) {
       double v = rtf[j];
       for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtf[i]));
@@ -167,23 +195,28 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
     }
   }
   __syncwarp();
-  return 0;
+  return fail;
 }
 
 // Middles: solve_z(start_level = BETA+1) (aqif.py:148-178, _kernels.py:175-225),
-// p = BETA .. s-1, records read outside-in through a cp.async ring.
-// Returns 0 or the 1-based breakdown level.
+// p = BETA .. s-1, records read outside-in through a cp.async ring.  Lane 0
+// of the group carries the top (row p) chain, lane 1 the bottom (row q)
+// chain.  Returns 0 or the 1-based breakdown level.
 template <int BETA, bool EXACT>
-__device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, int lane)
+__device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, int gl,
+                             bool alive)
 {
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
   constexpr int ZC = LcpSmem<BETA>::ZC;
   constexpr int RS = PL::kSize;
+  constexpr int G = Group<BETA>::G;
   const int s = n / 2;
   const int M = s - BETA;  // middle levels
+  const int sd = gl & 1;
+  const unsigned pair = 0x3u << ((threadIdx.x & 31) & ~1);
   double xl[BETA], xr[BETA];
-  if (lane == 0) {
+  if (alive && gl < 2) {
 #pragma unroll
     for (int j = 0; j < BETA; ++j) {
       xl[j] = x[j];
@@ -191,12 +224,14 @@ __device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, i
     }
   }
   auto issue = [&](int c0, int buf) {
-    const int k_hi = s - BETA - c0;
-    const int k_lo = max(1, k_hi - ZC + 1);
-    const int pieces = (k_hi - k_lo + 1) * RS / 2;
-    const double* src = zs + (size_t)k_lo * RS;
-    double* dst = ring + buf * ZC * RS;
-    for (int q = lane; q < pieces; q += 32) cp_async16(dst + 2 * q, src + 2 * q);
+    if (alive) {
+      const int k_hi = s - BETA - c0;
+      const int k_lo = max(1, k_hi - ZC + 1);
+      const int pieces = (k_hi - k_lo + 1) * RS / 2;
+      const double* src = zs + (size_t)k_lo * RS;
+      double* dst = ring + buf * ZC * RS;
+      for (int q = gl; q < pieces; q += G) cp_async16(dst + 2 * q, src + 2 * q);
+    }
     cp_async_commit();
   };
   int status = 0;
@@ -209,7 +244,7 @@ __device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, i
       cp_async_wait<0>();
     }
     __syncwarp();
-    if (lane == 0 && status == 0) {
+    if (alive && gl < 2 && status == 0) {
       const int k_hi = s - BETA - c0;
       const int k_lo = max(1, k_hi - ZC + 1);
       const double* buf = ring + cb * ZC * RS;
@@ -219,16 +254,15 @@ __device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, i
         if (p >= s) break;
         const int q = n - 1 - p, k = s - p;
         const double* rec = buf + (k - k_lo) * RS;
-        double rt = rec[PL::kYT], rb = rec[PL::kYB];
+        double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
 #pragma unroll
         for (int t = 0; t < BETA; ++t) {
-          const double xj = xl[(ph + t) % BETA];
-          rt = A::axpy_neg(rt, rec[PL::zi(0, BETA - t, 0)], xj);
-          rb = A::axpy_neg(rb, rec[PL::zi(0, BETA - t, 1)], xj);
-          const double xj2 = xr[(ph - 1 - t + 2 * BETA) % BETA];
-          rt = A::axpy_neg(rt, rec[PL::zi(1, 1 + t, 0)], xj2);
-          rb = A::axpy_neg(rb, rec[PL::zi(1, 1 + t, 1)], xj2);
+          acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
+          acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd], xr[(ph - 1 - t + 2 * BETA) % BETA]);
         }
+        const double oth = __shfl_xor_sync(pair, acc, 1);
+        const double rt = sd == 0 ? acc : oth;
+        const double rb = sd == 0 ? oth : acc;
         const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
         const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
         const double det = A::det2(a11, a22, a12, a21);
@@ -240,77 +274,105 @@ __device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, i
           status = p + 1;
           break;
         }
-        const double xp = A::div(A::det2(a22, rt, a12, rb), det);
-        const double xq = A::div(A::det2(a11, rb, a21, rt), det);
-        x[p] = xp;
-        x[q] = xq;
+        double xp, xq;
+        if (EXACT) {
+          const double y = __drcp_rn(det);
+          const bool ds = div_safe(det);
+          xp = div_rn(A::det2(a22, rt, a12, rb), det, y, ds);
+          xq = div_rn(A::det2(a11, rb, a21, rt), det, y, ds);
+        } else {
+          const double inv = 1.0 / det;
+          xp = (a22 * rt - a12 * rb) * inv;
+          xq = (a11 * rb - a21 * rt) * inv;
+        }
+        x[sd == 0 ? p : q] = sd == 0 ? xp : xq;
         xl[ph % BETA] = xp;
         xr[ph % BETA] = xq;
       }
     }
-    status = __shfl_sync(0xffffffffu, status, 0);
-    __syncwarp();
-    if (status) {
+    // group-uniform status (lane 0 of the group holds it)
+    status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
+    if (__all_sync(0xffffffffu, status != 0 || !alive)) {
       cp_async_wait<0>();
       break;
     }
+    __syncwarp();
   }
+  cp_async_wait<0>();
   __syncwarp();
   return status;
 }
 
 template <int BETA, bool EXACT, bool SOLVE_ONLY>
-__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock)
+__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 4)
 lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
            double tol, int max_outer, double* u_out, uint8_t* act_out, int64_t* passes_out,
-           double* res_out, int64_t* status_out, char* ws, size_t ws_per_warp, int total_warps)
+           double* res_out, int64_t* status_out, char* ws, size_t ws_per_slot, int total_warps)
 {
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
-  __shared__ __align__(16) LcpSmem<BETA> sm[kLcpWarpsPerBlock];
+  constexpr int G = Group<BETA>::G;
+  constexpr int P = Group<BETA>::P;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char lcp_dyn_smem[];
+  LcpSmem<BETA>* sm = reinterpret_cast<LcpSmem<BETA>*>(lcp_dyn_smem);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane / G, gl = lane % G;
   const int gw = blockIdx.x * kLcpWarpsPerBlock + wid;
   if (gw >= total_warps) return;
+  LcpSmem<BETA>& my_sm = sm[wid * P + g];
   const int s = n / 2;
   const size_t nb = (size_t)(2 * BETA + 1) * n;
-  char* my = ws + (size_t)gw * ws_per_warp;
+  char* my = ws + ((size_t)gw * P + g) * ws_per_slot;
   double* zs = reinterpret_cast<double*>(my);
   size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
   double* x = reinterpret_cast<double*>(my + off);
   off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
-  uint8_t* act = reinterpret_cast<uint8_t*>(my + off);
-  off += ((size_t)n + 255) & ~(size_t)255;
-  uint8_t* nact = reinterpret_cast<uint8_t*>(my + off);
+  uint32_t* act = reinterpret_cast<uint32_t*>(my + off);
+  off += ((size_t)n * 4 + 255) & ~(size_t)255;
+  uint32_t* nact = reinterpret_cast<uint32_t*>(my + off);
+#ifdef PAQIF_PROFILE_PHASES
+  unsigned long long ph_acc[4] = {0, 0, 0, 0};
+#endif
 
-  for (int64_t b = gw; b < B; b += total_warps) {
-    const double* bd = bands + b * nb;
-    const double* fb = f + b * (size_t)n;
-    double* ub = u_out + b * (size_t)n;
-    uint8_t* ab = SOLVE_ONLY ? nullptr : act_out + b * (size_t)n;
+  for (int64_t base = (int64_t)gw * P; base < B; base += (int64_t)total_warps * P) {
+    const int64_t b = base + g;
+    const bool have = b < B;
+    const double* bd = bands + (have ? b : 0) * nb;
+    const double* fb = f + (have ? b : 0) * (size_t)n;
+    double* ub = u_out + (have ? b : 0) * (size_t)n;
+    uint8_t* ab = SOLVE_ONLY ? nullptr : act_out + (have ? b : 0) * (size_t)n;
     double cmax = 0.0, fmax = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      const double fi = fb[i];
-      const uint8_t a = SOLVE_ONLY ? 0 : (fi <= 0.0);
-      act[i] = a;
-      if (!SOLVE_ONLY) {
-        ub[i] = 0.0;
-        ab[i] = a;
-        double c = 0.0;
-        for (int d = 0; d <= 2 * BETA; ++d) c = c + fabs(bd[(size_t)d * n + i]);
-        cmax = c > cmax ? c : cmax;
-        fmax = fabs(fi) > fmax ? fabs(fi) : fmax;
+    if (have) {
+      for (int i = gl; i < n; i += G) {
+        const double fi = fb[i];
+        const uint32_t a = SOLVE_ONLY ? 0u : (fi <= 0.0 ? 1u : 0u);
+        act[i] = a;
+        if (!SOLVE_ONLY) {
+          ub[i] = 0.0;
+          ab[i] = (uint8_t)a;
+          double c = 0.0;
+          for (int d = 0; d <= 2 * BETA; ++d) c = c + fabs(bd[(size_t)d * n + i]);
+          cmax = c > cmax ? c : cmax;
+          fmax = fabs(fi) > fmax ? fabs(fi) : fmax;
+        }
       }
     }
-    cmax = warp_max(cmax);
-    fmax = warp_max(fmax);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      cmax = fmax_(cmax, __shfl_xor_sync(FULL, cmax, o));
+      fmax = fmax_(fmax, __shfl_xor_sync(FULL, fmax, o));
+    }
     const double floor_ = 1e3 * DBL_EPSILON * (cmax + fmax);
     const double lim = tol > floor_ ? tol : floor_;
     double best_res = INFINITY, res = INFINITY;
     int passes = 0, st = 0;
     bool done = false;
-    uint8_t* cur = act;
-    uint8_t* nxt = nact;
+    bool active = have;  // this group still iterating
+    uint32_t* cur = act;
+    uint32_t* nxt = nact;
     for (int outer = 0; outer < max_outer; ++outer) {
+      if (!__any_sync(FULL, active)) break;
       __syncwarp();
       LcpPol<BETA> pol;
       pol.band = bd;
@@ -319,72 +381,115 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       pol.zs = zs;
       pol.n = n;
       pol.use_act = !SOLVE_ONLY;
-      passes = outer + 1;
-      if (aqif_factor_warp<BETA, EXACT>(pol, n, 1e-14, sm[wid].pbuf, lane)) {
+      if (active) passes = outer + 1;
+      PAQIF_TSTAMP(t0);
+      if (aqif_factor_group<BETA, EXACT>(pol, n, 1e-14, my_sm.eng, gl, active)) {
         st = PAQIF_LCP_FACTOR_BREAKDOWN;
-        break;
+        active = false;
       }
       __syncwarp();
-      if (corner_solve<BETA, EXACT>(zs, n, x, sm[wid].scratch, lane)) {
+      PAQIF_TSTAMP(t1);
+      if (corner_solve<BETA, EXACT>(zs, n, x, my_sm.post.scratch, gl, active)) {
         st = PAQIF_LCP_NOT_PD;
-        break;
+        active = false;
       }
-      if (zsolve_middle<BETA, EXACT>(zs, n, x, sm[wid].scratch, lane)) {
+      PAQIF_TSTAMP(t2);
+      if (zsolve_middle<BETA, EXACT>(zs, n, x, my_sm.post.scratch, gl, active)) {
         st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
-        break;
+        active = false;
       }
+      PAQIF_TSTAMP(t3);
+      PAQIF_TACC(0, t0, t1);
+      PAQIF_TACC(1, t1, t2);
+      PAQIF_TACC(2, t2, t3);
       if (SOLVE_ONLY) {
-        for (int i = lane; i < n; i += 32) ub[i] = x[i];
-        done = true;
-        break;
+        if (active) {
+          for (int i = gl; i < n; i += G) ub[i] = x[i];
+          done = true;
+        }
+        active = false;
+        continue;
       }
       // complementarity check and next policy (parallel.py:329-343)
       double r = 0.0;
       int changed = 0;
-      for (int i = lane; i < n; i += 32) {
-        double acc1 = 0.0, acc2 = 0.0;
-        const int lo = i - BETA > 0 ? i - BETA : 0;
-        const int hi = i + BETA + 1 < n ? i + BETA + 1 : n;
-        for (int j = lo; j < hi; ++j) {
-          const double a = bd[(size_t)(j - i + BETA) * n + i];
-          const double xe = x[j];
-          acc1 = A::axpy(acc1, a, xe);
-          acc2 = A::axpy(acc2, a, np_max0(xe));
+      if (active) {
+        for (int i = gl; i < n; i += G) {
+          double acc1 = 0.0, acc2 = 0.0;
+          if (i >= BETA && i < n - BETA) {
+            // interior row: all 2*BETA+1 terms, strided pointer walk
+            const double* pa = bd + i;
+            const double* px = x + (i - BETA);
+            double av[2 * BETA + 1], xv[2 * BETA + 1];
+#pragma unroll
+            for (int d = 0; d <= 2 * BETA; ++d) {
+              av[d] = __ldg(pa + (size_t)d * n);
+              xv[d] = px[d];
+            }
+#pragma unroll
+            for (int d = 0; d <= 2 * BETA; ++d) {
+              acc1 = A::axpy(acc1, av[d], xv[d]);
+              acc2 = A::axpy(acc2, av[d], np_max0(xv[d]));
+            }
+          } else {
+            const int lo = i - BETA > 0 ? i - BETA : 0;
+            const int hi = i + BETA + 1 < n ? i + BETA + 1 : n;
+            for (int j = lo; j < hi; ++j) {
+              const double a = bd[(size_t)(j - i + BETA) * n + i];
+              const double xe = x[j];
+              acc1 = A::axpy(acc1, a, xe);
+              acc2 = A::axpy(acc2, a, np_max0(xe));
+            }
+          }
+          const double xi = x[i];
+          const double lam = A::sub(acc1, fb[i]);
+          const double rr = A::sub(acc2, fb[i]);
+          const double mn = fabs(np_min(np_max0(xi), rr));
+          r = (r != r || mn != mn) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
+          const uint32_t na = xi < lam ? 1u : 0u;
+          nxt[i] = na;
+          changed |= (na != cur[i]);
         }
-        const double xi = x[i];
-        const double lam = A::sub(acc1, fb[i]);
-        const double rr = A::sub(acc2, fb[i]);
-        const double mn = fabs(np_min(np_max0(xi), rr));
-        r = (r != r || mn != mn) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
-        const uint8_t na = xi < lam;
-        nxt[i] = na;
-        changed |= (na != cur[i]);
       }
-      r = warp_max(r);
-      changed = __any_sync(0xffffffffu, changed);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(FULL, r, o);
+        r = (r != r || w != w) ? __longlong_as_double(0x7ff8000000000000ll) : (w > r ? w : r);
+        changed |= __shfl_xor_sync(FULL, changed, o);
+      }
+      PAQIF_TSTAMP(t4);
+      PAQIF_TACC(3, t3, t4);
+      if (!active) continue;
       res = r;
       if (res <= tol || res < best_res) {
-        for (int i = lane; i < n; i += 32) {
+        for (int i = gl; i < n; i += G) {
           ub[i] = np_max0(x[i]);
-          ab[i] = cur[i];
+          ab[i] = (uint8_t)cur[i];
         }
         if (res <= tol) {
           done = true;
-          break;
+          active = false;
+          continue;
         }
         best_res = res;
       }
-      if (!changed) break;
-      uint8_t* t = cur;
+      if (!changed) {
+        active = false;
+        continue;
+      }
+      uint32_t* t = cur;
       cur = nxt;
       nxt = t;
     }
-    if (!done && st == 0) {
+    if (have && !done && st == 0) {
       if (best_res <= lim) res = best_res;
       else st = PAQIF_LCP_NONCONVERGED;
     }
     __syncwarp();
-    if (lane == 0) {
+    if (have && gl == 0) {
+#ifdef PAQIF_PROFILE_PHASES
+      for (int q = 0; q < 4; ++q) { atomicAdd(&g_phase_cycles[q], ph_acc[q]); ph_acc[q] = 0; }
+#endif
       if (passes_out) passes_out[b] = passes;
       if (res_out) res_out[b] = res;
       status_out[b] = st;
@@ -393,13 +498,18 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
 }
 
 template <int BETA>
-size_t lcp_ws_per_warp(int n) {
+constexpr size_t lcp_smem_bytes() {
+  return sizeof(LcpSmem<BETA>) * kLcpWarpsPerBlock * Group<BETA>::P;
+}
+
+template <int BETA>
+size_t lcp_ws_per_slot(int n) {
   using PL = PivotLayout<BETA>;
   const int s = n / 2;
   size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
   off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
-  off += ((size_t)n + 255) & ~(size_t)255;
-  off += ((size_t)n + 255) & ~(size_t)255;
+  off += ((size_t)n * 4 + 255) & ~(size_t)255;
+  off += ((size_t)n * 4 + 255) & ~(size_t)255;
   return off;
 }
 
@@ -414,11 +524,15 @@ int lcp_grid_warps(int64_t B) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = lcp_smem_bytes<BETA>();
+  cudaFuncSetAttribute(lcp_kernel<BETA, EXACT, SOLVE_ONLY>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lcp_kernel<BETA, EXACT, SOLVE_ONLY>,
-                                                32 * kLcpWarpsPerBlock, 0);
+                                                32 * kLcpWarpsPerBlock, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t w = (int64_t)sms * per_sm * kLcpWarpsPerBlock;
-  if (w > B) w = B;
+  const int64_t need = (B + Group<BETA>::P - 1) / Group<BETA>::P;
+  if (w > need) w = need;
   return (int)(w < 1 ? 1 : w);
 }
 
@@ -442,14 +556,14 @@ struct LcpDispatch {
 template <int BETA, bool EXACT, bool SOLVE_ONLY>
 int run_lcp(const LcpDispatch& a) {
   const int warps = lcp_grid_warps<BETA, EXACT, SOLVE_ONLY>(a.B);
-  const size_t per = lcp_ws_per_warp<BETA>(a.n);
-  if (a.ws_bytes < per * (size_t)warps) {
-    std::snprintf(last_error_buf(), 512, "workspace too small: need %zu bytes",
-                  per * (size_t)warps);
+  const size_t per = lcp_ws_per_slot<BETA>(a.n);
+  const size_t need = per * (size_t)warps * Group<BETA>::P;
+  if (a.ws_bytes < need) {
+    std::snprintf(last_error_buf(), 512, "workspace too small: need %zu bytes", need);
     return PAQIF_E_WORKSPACE;
   }
   const unsigned grid = (unsigned)((warps + kLcpWarpsPerBlock - 1) / kLcpWarpsPerBlock);
-  lcp_kernel<BETA, EXACT, SOLVE_ONLY><<<grid, 32 * kLcpWarpsPerBlock, 0, a.st>>>(
+  lcp_kernel<BETA, EXACT, SOLVE_ONLY><<<grid, 32 * kLcpWarpsPerBlock, lcp_smem_bytes<BETA>(), a.st>>>(
       a.B, a.n, a.bands, a.f, a.tol, a.max_outer, a.u, a.act, a.passes, a.res, a.status,
       (char*)a.ws, per, warps);
   return check_launch("lcp_kernel");
@@ -476,7 +590,7 @@ size_t ws_bytes_for(int64_t B, int64_t n, int64_t beta, bool exact) {
   switch (beta) {
 #define PAQIF_WS_CASE(BB)                                                        \
   case BB:                                                                       \
-    per = lcp_ws_per_warp<BB>((int)n);                                           \
+    per = lcp_ws_per_slot<BB>((int)n) * Group<BB>::P;                            \
     warps = exact ? lcp_grid_warps<BB, true, false>(B) : lcp_grid_warps<BB, false, false>(B); \
     break;
     PAQIF_WS_CASE(1)
