@@ -1,0 +1,68 @@
+/*
+ * paqif_ehl.h -- C ABI of the fused EHL Newton steps (libpaqif_b200.so).
+ * Same conventions as paqif_b200.h (return codes, [dev] pointers, streams).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/paqif):
+ *   paqif_ehl_line_step   one outer iteration of ehl.solver.solve_ehl for the
+ *                         line contact, for B independent load cases:
+ *                         _line_contact_sweep (ehl/solver.py:131-183),
+ *                         force_balance_update (ehl/sweeps.py:521-535, when
+ *                         (outer+1) % force_every == 0) and
+ *                         EhlState.complementarity_residual (ehl/solver.py:43-51).
+ */
+#ifndef PAQIF_EHL_H
+#define PAQIF_EHL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Line-contact step configuration, common to the batch (EhlParams fields,
+ * ehl/params.py:40-58, plus the solve_ehl arguments). */
+typedef struct {
+  int32_t n;            /* grid intervals; nodes = n + 1                     */
+  int32_t limiter;      /* 0 kappa, 1 none, 2 van-albada, 3 minmod, 4 koren  */
+  int32_t variant;      /* 0 Lhs1 (Ls1/Ls4), 1 Lhs2 (Ls0/Ls5)                */
+  int32_t compressible; /* Dowson-Higginson + Roelands (1) or unit (0)       */
+  int32_t force_every;  /* force-balance period                              */
+  int32_t outer;        /* 0-based outer iteration index of this step        */
+  double h, lo;         /* spacing and left end of the domain                */
+  double kappa, omega, max_change, relax_c, max_h0_step, load_target;
+  double alpha, z, p0;  /* pressure-viscosity constants                      */
+} paqif_ehl_line_cfg;
+
+/* Workspace for paqif_ehl_line_step (B cases on n intervals). */
+size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n);
+
+/* One outer iteration for every case b (one CTA per case).
+ *   table   [dev] (n+1)      line kernel cell integrals (kernels.kernel_line)
+ *   p_hertz [dev] (B)        per-case p_H;  lam [dev] (B) per-case lambda
+ *   u       [dev] (B, n+1)   pressure in, updated pressure out
+ *   h0      [dev] (B)        offset in/out
+ *   film    [dev] (B, n+1)   film of the new state (out)
+ *   res     [dev] (B)        complementarity residual of the new state (out)
+ *   deficit [dev] (B)        load deficit target - h*sum(u) if the force balance
+ *                            ran this step, else NaN (out, may be NULL)
+ *   info    [dev] (B) int32  bits 0-1: solve rung (0 combined system, 1..3 Ls4
+ *                            ladder scheme / first-order / diagonal), bit 2:
+ *                            force balance applied, bit 3: non-finite change,
+ *                            bit 8: every rung broke down, bits 16..: number of
+ *                            weighted (eps/h <= 0.6) rows */
+int paqif_ehl_line_step(const paqif_ehl_line_cfg *cfg, int64_t B, const double *table,
+                        const double *p_hertz, const double *lam, double *u, double *h0,
+                        double *film, double *res, double *deficit, int32_t *info,
+                        uint32_t flags, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Line deformation  d_b[i] = -(1/pi) sum_j table[|i-j|] u_b[j]  for B pressure
+ * vectors of n+1 nodes (FilmModel.deformation_full, ehl/film.py:67-71). */
+int paqif_line_deformation(int64_t B, int64_t n, const double *table /*[dev] n+1*/,
+                           const double *u /*[dev] (B, n+1)*/, double *out /*[dev] (B, n+1)*/,
+                           void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAQIF_EHL_H */

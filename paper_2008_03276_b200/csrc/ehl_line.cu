@@ -1,0 +1,581 @@
+// Fused EHL line-contact Newton step (configs 1 and 3): one CTA per load
+// case runs one complete outer iteration of solve_ehl for the line contact
+// (paqif/ehl/solver.py:131-183 + 217-222 + 43-51):
+//
+//   film    = h0 + x^2/2 - (1/pi) sum_j K|i-j| u_j     deformation, film.py:67-71
+//   rho, eta, eps = rheology(u, film)                  params.py:149-175
+//   q = rho film; limited faces phi+, phi-; flux diff  sweeps.py:47-56, 89-103
+//   resid = (e+ (u_E-u_P) + e- (u_W-u_P))/h - fdiff   solver.py:144-149
+//   Ls1 / Ls4 pentadiagonal Jacobians + bad-row fix,
+//   row merge by the weighted mask eps/h <= 0.6        sweeps.py:157-267, solver.py:153-162
+//   AQIF solve (factor + W fused, Z outside-in); on a
+//   breakdown the Ls4 ladder scheme/first-order/diag   sweeps.py:270-295, solver.py:163-168
+//   clip, weighted spread, u = max(0, u + w(s - sp/4))  solver.py:169-181
+//   deformation of the new pressure                    solver.py:182
+//   force balance every force_every-th iteration       sweeps.py:521-535
+//   complementarity residual max|min(u, -R)|/h         solver.py:43-51
+//
+// The Toeplitz convolution is register-tiled (4 outputs per thread, one
+// shared-memory kernel value and one broadcast pressure per 4 DFMA); the
+// banded solve runs on one warp through the same AQIF engine as the LCP
+// path (aqif_warp.cuh) with the line system staged in the case's
+// workspace.  Elementwise formulas follow numpy's operation order; the
+// convolution and the load sum use a different summation order than
+// numpy's BLAS dot / pairwise sum (documented tolerance).
+#include <cfloat>
+#include "aqif_warp.cuh"
+#include "zsolve.cuh"
+#include "capi_util.cuh"
+
+namespace paqif {
+
+constexpr int kEhlThreads = 256;
+constexpr int kEhlBeta = 2;
+constexpr double kDensA = 0.59e9;
+constexpr double kDensB = 1.34;
+constexpr double kRatioGuard = 1e-30;
+constexpr double kSwitch = 0.6;
+
+struct EhlLinePol {
+  static constexpr bool kFuseW = true;
+  static constexpr bool kResidual = false;
+  static constexpr bool kRecordW = false;
+  using PL = PivotLayout<kEhlBeta>;
+  const double* band;
+  const double* rhs;
+  double* zs;
+  int n;
+  __device__ __forceinline__ const double* raw_ptr(int i, int d) const {
+    return band + (size_t)(d + kEhlBeta) * n + i;
+  }
+  __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
+  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
+  __device__ __forceinline__ bool pinned(int) const { return false; }
+  __device__ __forceinline__ const double* frhs_ptr(int i) const { return rhs + i; }
+  __device__ __forceinline__ double frhs(int i) const { return rhs[i]; }
+  __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
+    double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
+    const double2* src = reinterpret_cast<const double2*>(pb);
+    for (int idx = gl; idx < PL::kSize / 2; idx += G) dst[idx] = src[idx];
+  }
+  __device__ __forceinline__ void on_w(int, int, double, double) {}
+  __device__ __forceinline__ void on_resid(int, int, double) {}
+};
+
+// ---------------------------------------------------------------- limiters
+// tvdcd.limiter_psi / limiter_weight_plus (tvdcd.py:207-235)
+__device__ __forceinline__ double np_maximum(double a, double b) {
+  return (a >= b || a != a) ? a : b;
+}
+__device__ __forceinline__ double np_minimum(double a, double b) {
+  return (a <= b || a != a) ? a : b;
+}
+__device__ double limiter_psi(double r, int name, double kappa) {
+  switch (name) {
+    case 1:  // none
+      return ((1.0 + kappa) * r + (1.0 - kappa)) / 2.0;
+    case 2:  // van-albada
+      return r > 0.0 ? (r * r + r) / (1.0 + r * r) : 0.0;
+    case 3:  // minmod
+      return np_maximum(0.0, np_minimum(r, 1.0));
+    case 4:  // koren
+      return np_maximum(0.0, np_minimum(np_minimum(2.0 * r, (1.0 + 2.0 * r) / 3.0), 2.0));
+    default: {  // kappa
+      const double lin = ((1.0 + kappa) * r + (1.0 - kappa)) / 2.0;
+      return np_maximum(0.0, np_minimum(np_minimum(2.0 * r, lin), 2.0));
+    }
+  }
+}
+__device__ __forceinline__ double limiter_wplus(double r, int name, double kappa) {
+  const double psi = limiter_psi(r, name, kappa);
+  const double safe = fabs(r) > kRatioGuard ? r : (r >= 0.0 ? kRatioGuard : -kRatioGuard);
+  return r > 0.0 ? psi / safe : 0.0;
+}
+// sweeps._guarded_ratio with a data scale (sweeps.py:47-56)
+__device__ __forceinline__ double gratio(double num, double den, double floor_) {
+  return fabs(den) > floor_ ? num / den : 0.0;
+}
+
+// ---------------------------------------------------------------- block helpers
+__device__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+  __syncthreads();
+  return r;
+}
+// NaN-propagating max (numpy max)
+__device__ double block_nanmax(double v, double* red) {
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = (v != v || w != w) ? qnan : (w > v ? w : v);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    const double x = red[w];
+    r = (r != r || x != x) ? qnan : (x > r ? x : r);
+  }
+  __syncthreads();
+  return r;
+}
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += red[w];
+  __syncthreads();
+  return r;
+}
+
+// deformation: def[i] = sign * sum_j u[j] * ext[n + i - j], i = 0..n
+// (np.convolve(u, ext)[n:2n+1]); 4 consecutive outputs per thread
+__device__ void toeplitz_conv(const double* su, const double* ext, int n, double sign,
+                              double* out) {
+  const int N = n + 1;
+  for (int i0 = 4 * threadIdx.x; i0 < N; i0 += 4 * blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    // e_r = ext[n + i0 + r - j]; slide as j increases
+    const double* eb = ext + n + i0;
+    double e0 = eb[0], e1 = eb[1], e2 = eb[2], e3 = eb[3];
+    for (int j = 0; j < N; ++j) {
+      const double uj = su[j];
+      a0 = fma(uj, e0, a0);
+      a1 = fma(uj, e1, a1);
+      a2 = fma(uj, e2, a2);
+      a3 = fma(uj, e3, a3);
+      e3 = e2;
+      e2 = e1;
+      e1 = e0;
+      e0 = eb[-j - 1];
+    }
+    out[i0] = sign * a0;
+    if (i0 + 1 < N) out[i0 + 1] = sign * a1;
+    if (i0 + 2 < N) out[i0 + 2] = sign * a2;
+    if (i0 + 3 < N) out[i0 + 3] = sign * a3;
+  }
+}
+
+struct EhlSmemLayout {
+  // offsets in doubles
+  int ext, su, sun, film, rho, eps, q, php, phm, res, sig, def, red, eng, ring, total;
+  __host__ __device__ explicit EhlSmemLayout(int n) {
+    const int N = n + 1, NA = (N + 3 + 1) & ~1;  // padded for the 4-wide conv tail
+    int o = 0;
+    ext = o + 8; o += 2 * n + 1 + 16; o = (o + 1) & ~1;  // 8-element guards both ends
+    su = o; o += NA;
+    sun = o; o += NA;
+    film = o; o += NA;
+    rho = o; o += NA;
+    eps = o; o += NA;
+    q = o; o += NA;
+    php = o; o += NA;
+    phm = o; o += NA;
+    res = o; o += NA;
+    sig = o; o += NA;
+    def = o; o += NA;
+    red = o; o += 32;
+    eng = o; o += (int)(sizeof(EngineSmem<kEhlBeta>) / 8) + 2;
+    ring = o; o += ZChunk<kEhlBeta>::kRing;
+    total = o;
+  }
+};
+
+}  // namespace paqif
+
+// ----------------------------------------------------------------- C ABI cfg
+extern "C" {
+#include "../../include/paqif_ehl.h"
+}
+
+namespace paqif {
+
+__device__ __forceinline__ void rheology(double u, double film, const paqif_ehl_line_cfg& c,
+                                         double ph, double lam, double& rho, double& eps) {
+  double eta;
+  if (c.compressible) {
+    const double p = u * ph;
+    rho = (kDensA + kDensB * p) / (kDensA + p);
+    const double arg = (c.alpha * c.p0 / c.z) * (-1.0 + pow(1.0 + p / c.p0, c.z));
+    eta = exp(np_minimum(arg, 200.0));
+  } else {
+    rho = 1.0;
+    eta = 1.0;
+  }
+  const double coeff = rho / (eta * lam);
+  const double gap = np_maximum(film, 1e-8);
+  eps = coeff * (gap * gap * gap);
+}
+
+// Assemble row r (interior node i = r+1) of the change system in the
+// requested scheme / Jacobian mode; writes the 5 band entries.
+// jac: 0 scheme, 1 first-order, 2 diagonal.  weighted: Ls4/Ls5 pattern.
+__device__ void assemble_row(int i, const double* rho, const double* eps, const double* php,
+                             const double* phm, double h, bool weighted, int jac, double ks0,
+                             double ks1, double* e /*[5]*/) {
+  const double rw = rho[i - 1], rc = rho[i], re = rho[i + 1];
+  const double ex_p = 0.5 * (eps[i] + eps[i + 1]);
+  const double ex_m = 0.5 * (eps[i] + eps[i - 1]);
+  double phi_p = php[i], phi_m = phm[i];
+  if (jac != 0) {
+    phi_p = 0.0;
+    phi_m = 0.0;
+  }
+  const double a_p = 1.0 - 0.5 * phi_p, b_p = 0.5 * phi_p;
+  const double a_m = 1.0 - 0.5 * phi_m, b_m = 0.5 * phi_m;
+  const double hy = 1.0;
+  double c_m2, c_m1, c_0, c_p1, c_p2;
+  if (jac == 2) {
+    c_m2 = 0.0; c_m1 = 0.0; c_p1 = 0.0; c_p2 = 0.0;
+    c_0 = -hy * rc * fabs(ks0);
+  } else {
+    c_m2 = hy * (a_m * rw * ks1);
+    c_m1 = -hy * (a_p * rc * ks1 - a_m * rw * ks0 - b_m * rc * ks1);
+    c_0 = -hy * (a_p * rc * ks0 + b_p * re * ks1 - a_m * rw * ks1 - b_m * rc * ks0);
+    c_p1 = -hy * (a_p * rc * ks1 + b_p * re * ks0 - b_m * rc * ks1);
+    c_p2 = -hy * (b_p * re * ks1);
+  }
+  const double ey_sum = 0.0 + 0.0;
+  double p_m2, p_m1, p_0, p_p1, p_p2;
+  if (weighted) {
+    p_m2 = -0.25 * ex_m / h;
+    p_m1 = (1.25 * ex_m + 0.25 * ex_p) / h + 0.25 * ey_sum / h;
+    p_0 = -1.25 * (ex_p + ex_m + ey_sum) / h;
+    p_p1 = (1.25 * ex_p + 0.25 * ex_m) / h + 0.25 * ey_sum / h;
+    p_p2 = -0.25 * ex_p / h;
+  } else {
+    p_m2 = 0.0;
+    p_m1 = ex_m / h;
+    p_0 = -(ex_p + ex_m + ey_sum) / h;
+    p_p1 = ex_p / h;
+    p_p2 = 0.0;
+  }
+  e[0] = -(c_m2 + p_m2);
+  e[1] = -(c_m1 + p_m1);
+  e[2] = -(c_0 + p_0);
+  e[3] = -(c_p1 + p_p1);
+  e[4] = -(c_p2 + p_p2);
+  const double off_mag = fabs(e[0]) + fabs(e[1]) + fabs(e[3]) + fabs(e[4]);
+  const double floor_ = 0.05 * hy * fabs(rc) * fabs(ks0);
+  if (fabs(e[2]) < np_maximum(0.2 * off_mag, floor_)) {
+    const double fo_m2 = hy * rw * ks1;
+    const double fo_m1 = -hy * (rc * ks1 - rw * ks0);
+    const double fo_0 = -hy * (rc * ks0 - rw * ks1);
+    const double fo_p1 = -hy * rc * ks1;
+    e[0] = -(fo_m2 + p_m2);
+    e[1] = -(fo_m1 + p_m1);
+    e[2] = -(fo_0 + p_0);
+    e[3] = -(fo_p1 + p_p1);
+    e[4] = -p_p2;
+  }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kEhlThreads)
+ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
+                const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
+                double* h0_io, double* film_out, double* res_out, double* deficit_out,
+                int32_t* info_out, char* ws, size_t ws_per_case)
+{
+  extern __shared__ __align__(16) double esm[];
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int n = c.n, N = n + 1, n_int = n - 1;
+  const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+  const EhlSmemLayout L(n);
+  double* ext = esm + L.ext;
+  double* su = esm + L.su;
+  double* sun = esm + L.sun;
+  double* sfilm = esm + L.film;
+  double* srho = esm + L.rho;
+  double* seps = esm + L.eps;
+  double* sq = esm + L.q;
+  double* sphp = esm + L.php;
+  double* sphm = esm + L.phm;
+  double* sres = esm + L.res;
+  double* ssig = esm + L.sig;
+  double* sdef = esm + L.def;
+  double* red = esm + L.red;
+  EngineSmem<kEhlBeta>& eng = *reinterpret_cast<EngineSmem<kEhlBeta>*>(esm + L.eng);
+  double* ring = esm + L.ring;
+  // workspace of this case
+  char* my = ws + (size_t)b * ws_per_case;
+  double* band = reinterpret_cast<double*>(my);
+  double* rhs = band + (size_t)(2 * kEhlBeta + 1) * n_sys;
+  double* xsol = rhs + n_sys;
+  double* zs = xsol + n_sys;
+  const double ph = p_hertz[b], lam = lamv[b];
+  const double h = c.h;
+  const double sign = -1.0 / 3.141592653589793;
+  double h0 = h0_io[b];
+
+  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
+  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
+    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  __syncthreads();
+
+  // ---- film, rheology, faces, residual of the current pressure
+  toeplitz_conv(su, ext, n, 1.0, sdef);
+  __syncthreads();
+  double qmax = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double x = c.lo + h * (double)i;
+    const double fv = (h0 + 0.5 * (x * x)) + sign * sdef[i];
+    double rho, eps;
+    rheology(su[i], fv, c, ph, lam, rho, eps);
+    sfilm[i] = fv;
+    srho[i] = rho;
+    seps[i] = eps;
+    sq[i] = rho * fv;
+    qmax = fmax(qmax, fabs(rho * fv));
+  }
+  const double gfloor = 1e-12 * fmax(block_max(qmax, red), kRatioGuard);
+  for (int i = 1 + threadIdx.x; i < n; i += blockDim.x) {
+    const double dqi = sq[i + 1] - sq[i], dqm = sq[i] - sq[i - 1];
+    const double php = limiter_wplus(gratio(dqi, dqm, gfloor), c.limiter, c.kappa);
+    double phm = 0.0;
+    if (i >= 2) {
+      const double dqmm = sq[i - 1] - sq[i - 2];
+      phm = limiter_wplus(gratio(dqm, dqmm, gfloor), c.limiter, c.kappa);
+    }
+    sphp[i] = php;
+    sphm[i] = phm;
+    const double fd = (sq[i] + 0.5 * php * dqi) - (sq[i - 1] + 0.5 * phm * dqm);
+    const double e_p = 0.5 * (seps[i] + seps[i + 1]);
+    const double e_m = 0.5 * (seps[i] + seps[i - 1]);
+    sres[i] = (e_p * (su[i + 1] - su[i]) + e_m * (su[i - 1] - su[i])) / h - fd;
+  }
+  __syncthreads();
+
+  // kernel sensitivities (film.sensitivity, sweeps.kernel_nu)
+  const double s0 = sign * table[0], s1 = sign * table[1], s2 = sign * table[2];
+  const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
+                                   : (2.0 - c.kappa) / 2.0 + (1.0 - c.kappa) / 4.0;
+  const double ks0n = s0, ks1n = s1;
+  const double ks0w = nu * (s0 - 0.25 * (2.0 * s1 + 0.0));
+  const double ks1w = nu * (s1 - 0.25 * (s0 + s2 + 0.0));
+
+  // rung -1: combined (per-row Ls1/Ls4); 0..2: Ls4 with scheme/first-order/diagonal
+  int rung = -1;
+  int st = 1;
+  int weighted_rows = 0;
+  for (; rung <= 2; ++rung) {
+    int wcount = 0;
+    for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
+      double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
+      double rr = 0.0;
+      if (r < n_int) {
+        const int i = r + 1;
+        const bool wrow = (seps[i] / h) <= kSwitch;
+        wcount += wrow;
+        const bool weighted = rung >= 0 || wrow;
+        assemble_row(i, srho, seps, sphp, sphm, h, weighted, rung < 0 ? 0 : rung,
+                     weighted ? ks0w : ks0n, weighted ? ks1w : ks1n, e);
+        rr = sres[i];
+      }
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        const int col = r + d - kEhlBeta;
+        // padded-matrix semantics: rows beyond n_int are identity; entries
+        // leaving the (padded) matrix are exact zeros
+        const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (d == kEhlBeta);
+        band[(size_t)d * n_sys + r] = keep ? e[d] : 0.0;
+      }
+      rhs[r] = rr;
+    }
+    if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
+    __syncthreads();
+    // solve on warp 0 (group 0 of the engine; the other groups idle)
+    int fst = 0, zst = 0;
+    if (threadIdx.x < 32) {
+      constexpr int G = Group<kEhlBeta>::G;
+      const int lane = threadIdx.x;
+      const bool alive = lane < G;
+      EhlLinePol pol{band, rhs, zs, n_sys};
+      fst = aqif_factor_group<kEhlBeta, EXACT>(pol, n_sys, 1e-14, eng, lane % G, alive);
+      fst = __shfl_sync(0xffffffffu, fst, 0);
+      if (fst == 0) {
+        zst = zsolve_group<kEhlBeta, EXACT, true>(zs, n_sys, xsol, ring, lane % G, alive);
+        zst = __shfl_sync(0xffffffffu, zst, 0);
+      }
+      if (lane == 0) red[31] = (fst || zst) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    st = red[31] != 0.0;
+    __syncthreads();
+    if (!st) break;
+  }
+  if (st) {
+    // every rung broke down: the reference re-raises (robust_line_solve)
+    if (threadIdx.x == 0) {
+      res_out[b] = __longlong_as_double(0x7ff8000000000000ll);
+      if (deficit_out) deficit_out[b] = __longlong_as_double(0x7ff8000000000000ll);
+      info_out[b] = 1 << 8;
+    }
+    return;
+  }
+
+  // ---- update (solver.py:169-181)
+  bool finite = true;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double sg = 0.0;
+    if (i >= 1 && i <= n - 1) {
+      sg = xsol[i - 1];
+      finite &= isfinite(sg);
+      sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
+    }
+    ssig[i] = sg;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    auto wsig = [&](int k) -> double {
+      if (k < 1 || k > n - 1) return 0.0;
+      return (seps[k] / h) <= kSwitch ? ssig[k] : 0.0;
+    };
+    const double spread = (0.0 + (i >= 1 ? wsig(i - 1) : 0.0)) + (i < n ? wsig(i + 1) : 0.0);
+    const double v = su[i] + c.omega * (ssig[i] - 0.25 * spread);
+    sun[i] = (i == 0 || i == n) ? 0.0 : np_maximum(0.0, v);
+  }
+  const int fin_all = __syncthreads_and(finite);
+  // ---- deformation of the new pressure, force balance, residual
+  toeplitz_conv(sun, ext, n, 1.0, sdef);
+  __syncthreads();
+  int fb = 0;
+  double deficit_v = __longlong_as_double(0x7ff8000000000000ll);
+  if ((c.outer + 1) % c.force_every == 0) {
+    double part = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) part += sun[i];
+    const double total = block_sum(part, red);
+    const double deficit = c.load_target - h * total;
+    const double stp = np_minimum(np_maximum(c.relax_c * deficit, -c.max_h0_step), c.max_h0_step);
+    h0 = h0 - stp;
+    fb = 1;
+    deficit_v = deficit;
+  }
+  qmax = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double x = c.lo + h * (double)i;
+    const double fv = (h0 + 0.5 * (x * x)) + sign * sdef[i];
+    double rho, eps;
+    rheology(sun[i], fv, c, ph, lam, rho, eps);
+    sfilm[i] = fv;
+    seps[i] = eps;
+    sq[i] = rho * fv;
+    qmax = fmax(qmax, fabs(rho * fv));
+  }
+  const double gfloor2 = 1e-12 * fmax(block_max(qmax, red), kRatioGuard);
+  double comp = 0.0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double r = 0.0;
+    if (i >= 1 && i <= n - 1) {
+      const double dqi = sq[i + 1] - sq[i], dqm = sq[i] - sq[i - 1];
+      const double php = limiter_wplus(gratio(dqi, dqm, gfloor2), c.limiter, c.kappa);
+      double phm = 0.0;
+      if (i >= 2) {
+        const double dqmm = sq[i - 1] - sq[i - 2];
+        phm = limiter_wplus(gratio(dqm, dqmm, gfloor2), c.limiter, c.kappa);
+      }
+      const double fd = (sq[i] + 0.5 * php * dqi) - (sq[i - 1] + 0.5 * phm * dqm);
+      const double e_p = 0.5 * (seps[i] + seps[i + 1]);
+      const double e_m = 0.5 * (seps[i] + seps[i - 1]);
+      r = (e_p * (sun[i + 1] - sun[i]) + e_m * (sun[i - 1] - sun[i])) / h - fd;
+    }
+    const double m = fabs(np_minimum(sun[i], -r));
+    comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+  }
+  const double cmax = block_nanmax(comp, red);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    u_io[b * N + i] = sun[i];
+    film_out[b * N + i] = sfilm[i];
+  }
+  if (threadIdx.x == 0) {
+    h0_io[b] = h0;
+    res_out[b] = cmax / h;
+    if (deficit_out) deficit_out[b] = deficit_v;
+    // info: bits 0-1 rung+1 (0 combined), bit 2 force balance applied,
+    // bit 3 non-finite change, bits 16.. weighted rows
+    info_out[b] = (rung + 1) | (fb << 2) | ((fin_all ? 0 : 1) << 3) | (weighted_rows << 16);
+  }
+}
+
+}  // namespace paqif
+
+using namespace paqif;
+
+extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
+  if (B < 0 || n < 4) return 0;
+  const int64_t n_int = n - 1;
+  const int64_t n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+  const int64_t s = n_sys / 2;
+  const size_t per = ((size_t)(2 * kEhlBeta + 1) * n_sys + 2 * n_sys +
+                      (size_t)(s + 1) * PivotLayout<kEhlBeta>::kSize + 32) * 8;
+  return (size_t)B * ((per + 255) & ~(size_t)255);
+}
+
+extern "C" int paqif_ehl_line_step(const paqif_ehl_line_cfg* cfg, int64_t B, const double* table,
+                                   const double* p_hertz, const double* lam, double* u,
+                                   double* h0, double* film, double* res, double* deficit,
+                                   int32_t* info, uint32_t flags, void* workspace,
+                                   size_t workspace_bytes, void* stream)
+{
+  if (!cfg || B < 0 || cfg->n < 4 || cfg->force_every < 1) return set_arg_error("ehl_line: bad cfg");
+  if (B == 0) return PAQIF_OK;
+  const size_t need = paqif_ehl_line_workspace_bytes(B, cfg->n);
+  if (workspace_bytes < need) return set_arg_error("ehl_line: workspace too small");
+  const EhlSmemLayout L(cfg->n);
+  const size_t smem = (size_t)L.total * 8;
+  if (smem > 227 * 1024) return set_arg_error("ehl_line: grid too fine for one CTA");
+  const size_t per = need / (size_t)B;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (flags & PAQIF_FLAG_EXACT) {
+    cudaFuncSetAttribute(ehl_line_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ehl_line_kernel<true><<<(unsigned)B, kEhlThreads, smem, st>>>(
+        *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
+  } else {
+    cudaFuncSetAttribute(ehl_line_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ehl_line_kernel<false><<<(unsigned)B, kEhlThreads, smem, st>>>(
+        *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
+  }
+  return check_launch("paqif_ehl_line_step");
+}
+
+namespace paqif {
+__global__ void __launch_bounds__(kEhlThreads)
+line_deformation_kernel(int n, const double* __restrict__ table, const double* __restrict__ u,
+                        double* out)
+{
+  extern __shared__ __align__(16) double dsm[];
+  const int N = n + 1;
+  double* ext = dsm + 8;
+  double* su = dsm + 2 * n + 1 + 16;
+  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
+    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u[(size_t)blockIdx.x * N + k];
+  __syncthreads();
+  toeplitz_conv(su, ext, n, -1.0 / 3.141592653589793, out + (size_t)blockIdx.x * N);
+}
+}  // namespace paqif
+
+extern "C" int paqif_line_deformation(int64_t B, int64_t n, const double* table, const double* u,
+                                      double* out, void* stream)
+{
+  if (B < 0 || n < 1) return set_arg_error("line_deformation: bad sizes");
+  if (B == 0) return PAQIF_OK;
+  const size_t smem = (size_t)(2 * n + 1 + 16 + n + 1 + 8) * 8;
+  if (smem > 227 * 1024) return set_arg_error("line_deformation: grid too fine");
+  cudaFuncSetAttribute(line_deformation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  line_deformation_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>((int)n, table, u, out);
+  return check_launch("paqif_line_deformation");
+}

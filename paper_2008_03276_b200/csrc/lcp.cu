@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <mutex>
 #include "aqif_warp.cuh"
+#include "zsolve.cuh"
 #include "capi_util.cuh"
 
 namespace paqif {
@@ -83,7 +84,7 @@ __device__ unsigned long long g_phase_cycles[4];
 template <int BETA>
 struct LcpSmem {
   using PL = PivotLayout<BETA>;
-  static constexpr int ZC = BETA * ((8 + BETA - 1) / BETA);  // chunk, multiple of BETA
+  static constexpr int ZC = ZChunk<BETA>::ZC;
   static constexpr int kM = 2 * BETA;
   static constexpr int kCorner = 2 * kM * kM + 2 * kM;
   static constexpr int kRing = 2 * ZC * PL::kSize;
@@ -198,111 +199,6 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
   return fail;
 }
 
-// Middles: solve_z(start_level = BETA+1) (aqif.py:148-178, _kernels.py:175-225),
-// p = BETA .. s-1, records read outside-in through a cp.async ring.  Lane 0
-// of the group carries the top (row p) chain, lane 1 the bottom (row q)
-// chain.  Returns 0 or the 1-based breakdown level.
-template <int BETA, bool EXACT>
-__device__ int zsolve_middle(const double* zs, int n, double* x, double* ring, int gl,
-                             bool alive)
-{
-  using A = Arith<EXACT>;
-  using PL = PivotLayout<BETA>;
-  constexpr int ZC = LcpSmem<BETA>::ZC;
-  constexpr int RS = PL::kSize;
-  constexpr int G = Group<BETA>::G;
-  const int s = n / 2;
-  const int M = s - BETA;  // middle levels
-  const int sd = gl & 1;
-  const unsigned pair = 0x3u << ((threadIdx.x & 31) & ~1);
-  double xl[BETA], xr[BETA];
-  if (alive && gl < 2) {
-#pragma unroll
-    for (int j = 0; j < BETA; ++j) {
-      xl[j] = x[j];
-      xr[j] = x[n - 1 - j];
-    }
-  }
-  auto issue = [&](int c0, int buf) {
-    if (alive) {
-      const int k_hi = s - BETA - c0;
-      const int k_lo = max(1, k_hi - ZC + 1);
-      const int pieces = (k_hi - k_lo + 1) * RS / 2;
-      const double* src = zs + (size_t)k_lo * RS;
-      double* dst = ring + buf * ZC * RS;
-      for (int q = gl; q < pieces; q += G) cp_async16(dst + 2 * q, src + 2 * q);
-    }
-    cp_async_commit();
-  };
-  int status = 0;
-  if (M > 0) issue(0, 0);
-  for (int c0 = 0, cb = 0; c0 < M; c0 += ZC, cb ^= 1) {
-    if (c0 + ZC < M) {
-      issue(c0 + ZC, cb ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-    if (alive && gl < 2 && status == 0) {
-      const int k_hi = s - BETA - c0;
-      const int k_lo = max(1, k_hi - ZC + 1);
-      const double* buf = ring + cb * ZC * RS;
-#pragma unroll
-      for (int ph = 0; ph < ZC; ++ph) {
-        const int p = BETA + c0 + ph;
-        if (p >= s) break;
-        const int q = n - 1 - p, k = s - p;
-        const double* rec = buf + (k - k_lo) * RS;
-        double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
-#pragma unroll
-        for (int t = 0; t < BETA; ++t) {
-          acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
-          acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd], xr[(ph - 1 - t + 2 * BETA) % BETA]);
-        }
-        const double oth = __shfl_xor_sync(pair, acc, 1);
-        const double rt = sd == 0 ? acc : oth;
-        const double rb = sd == 0 ? oth : acc;
-        const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
-        const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
-        const double det = A::det2(a11, a22, a12, a21);
-        double scale = fabs(a11);
-        if (fabs(a12) > scale) scale = fabs(a12);
-        if (fabs(a21) > scale) scale = fabs(a21);
-        if (fabs(a22) > scale) scale = fabs(a22);
-        if (fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY) {
-          status = p + 1;
-          break;
-        }
-        double xp, xq;
-        if (EXACT) {
-          const double y = __drcp_rn(det);
-          const bool ds = div_safe(det);
-          xp = div_rn(A::det2(a22, rt, a12, rb), det, y, ds);
-          xq = div_rn(A::det2(a11, rb, a21, rt), det, y, ds);
-        } else {
-          const double inv = 1.0 / det;
-          xp = (a22 * rt - a12 * rb) * inv;
-          xq = (a11 * rb - a21 * rt) * inv;
-        }
-        x[sd == 0 ? p : q] = sd == 0 ? xp : xq;
-        xl[ph % BETA] = xp;
-        xr[ph % BETA] = xq;
-      }
-    }
-    // group-uniform status (lane 0 of the group holds it)
-    status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
-    if (__all_sync(0xffffffffu, status != 0 || !alive)) {
-      cp_async_wait<0>();
-      break;
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  __syncwarp();
-  return status;
-}
-
 template <int BETA, bool EXACT, bool SOLVE_ONLY>
 __global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 4)
 lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
@@ -394,7 +290,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         active = false;
       }
       PAQIF_TSTAMP(t2);
-      if (zsolve_middle<BETA, EXACT>(zs, n, x, my_sm.post.scratch, gl, active)) {
+      if (zsolve_group<BETA, EXACT, false>(zs, n, x, my_sm.post.scratch, gl, active)) {
         st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
         active = false;
       }

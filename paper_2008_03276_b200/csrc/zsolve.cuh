@@ -1,0 +1,143 @@
+// Outside-in Z solve for one system per lane group, reading the per-level
+// pivot records (PivotLayout, written by aqif_factor_group's policy) back
+// through a double-buffered cp.async ring in shared memory.  Lane 0 of the
+// group carries the top (row p) chain, lane 1 the bottom (row q) chain, in
+// the reference's operation order (solve_z_batch, paqif/_kernels.py:175-225).
+//
+//   FULL = false: solve_z(start_level = BETA+1) -- the PAQIF middles after
+//                 the corner system (parallel.py:234-258); x[0..BETA) and
+//                 x[n-BETA..n) are prefilled.
+//   FULL = true : solve_z(start_level = 1) -- a plain AQIF solve (the EHL
+//                 line solves, ehl/sweeps.py:270-273).
+#pragma once
+#include "aqif_warp.cuh"
+
+namespace paqif {
+
+template <int BETA>
+struct ZChunk {
+  static constexpr int ZC = BETA * ((8 + BETA - 1) / BETA);  // levels per chunk, multiple of BETA
+  static constexpr int kRing = 2 * ZC * PivotLayout<BETA>::kSize;  // doubles
+};
+
+// One level of the chains; CHECK enables the boundary skips of the first
+// BETA levels of a full solve.  Returns false on breakdown.
+template <int BETA, bool EXACT, bool CHECK>
+__device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, double& xp,
+                                       double& xq, const double* xl, const double* xr, int ph,
+                                       unsigned pair)
+{
+  using A = Arith<EXACT>;
+  using PL = PivotLayout<BETA>;
+  const int q = n - 1 - p;
+  double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
+#pragma unroll
+  for (int t = 0; t < BETA; ++t) {
+    if (!CHECK || p - BETA + t >= 0)
+      acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
+    if (!CHECK || q + 1 + t < n)
+      acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd],
+                        xr[(ph - 1 - t + 2 * BETA) % BETA]);
+  }
+  const double oth = __shfl_xor_sync(pair, acc, 1);
+  const double rt = sd == 0 ? acc : oth;
+  const double rb = sd == 0 ? oth : acc;
+  const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
+  const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
+  const double det = A::det2(a11, a22, a12, a21);
+  double scale = fabs(a11);
+  if (fabs(a12) > scale) scale = fabs(a12);
+  if (fabs(a21) > scale) scale = fabs(a21);
+  if (fabs(a22) > scale) scale = fabs(a22);
+  if (fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY) return false;
+  if (EXACT) {
+    const double y = __drcp_rn(det);
+    const bool ds = div_safe(det);
+    xp = div_rn(A::det2(a22, rt, a12, rb), det, y, ds);
+    xq = div_rn(A::det2(a11, rb, a21, rt), det, y, ds);
+  } else {
+    const double inv = 1.0 / det;
+    xp = (a22 * rt - a12 * rb) * inv;
+    xq = (a11 * rb - a21 * rt) * inv;
+  }
+  return true;
+}
+
+// All 32 lanes call.  Returns 0 or the 1-based breakdown level.
+template <int BETA, bool EXACT, bool FULL>
+__device__ int zsolve_group(const double* zs, int n, double* x, double* ring, int gl, bool alive)
+{
+  using PL = PivotLayout<BETA>;
+  constexpr int ZC = ZChunk<BETA>::ZC;
+  constexpr int RS = PL::kSize;
+  constexpr int G = Group<BETA>::G;
+  const int s = n / 2;
+  const int p0 = FULL ? 0 : BETA;  // first unknown pair solved
+  const int M = s - p0;            // levels to solve
+  const int sd = gl & 1;
+  const unsigned pair = 0x3u << ((threadIdx.x & 31) & ~1);
+  double xl[BETA], xr[BETA];
+  if (alive && gl < 2) {
+#pragma unroll
+    for (int j = 0; j < BETA; ++j) {
+      xl[j] = FULL ? 0.0 : x[j];
+      xr[j] = FULL ? 0.0 : x[n - 1 - j];
+    }
+  }
+  auto issue = [&](int c0, int buf) {
+    if (alive) {
+      const int k_hi = s - p0 - c0;
+      const int k_lo = max(1, k_hi - ZC + 1);
+      const int pieces = (k_hi - k_lo + 1) * RS / 2;
+      const double* src = zs + (size_t)k_lo * RS;
+      double* dst = ring + buf * ZC * RS;
+      for (int q = gl; q < pieces; q += G) cp_async16(dst + 2 * q, src + 2 * q);
+    }
+    cp_async_commit();
+  };
+  int status = 0;
+  if (M > 0) issue(0, 0);
+  for (int c0 = 0, cb = 0; c0 < M; c0 += ZC, cb ^= 1) {
+    if (c0 + ZC < M) {
+      issue(c0 + ZC, cb ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    if (alive && gl < 2 && status == 0) {
+      const int k_hi = s - p0 - c0;
+      const int k_lo = max(1, k_hi - ZC + 1);
+      const double* buf = ring + cb * ZC * RS;
+#pragma unroll
+      for (int ph = 0; ph < ZC; ++ph) {
+        const int p = p0 + c0 + ph;
+        if (p >= s) break;
+        const double* rec = buf + (s - p - k_lo) * RS;
+        double xp, xq;
+        const bool ok = (FULL && p < BETA)
+                            ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
+                            : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
+        if (!ok) {
+          status = p + 1;
+          break;
+        }
+        x[sd == 0 ? p : n - 1 - p] = sd == 0 ? xp : xq;
+        xl[ph % BETA] = xp;
+        xr[ph % BETA] = xq;
+      }
+    }
+    // group-uniform status (lane 0 of the group holds it)
+    status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
+    if (__all_sync(0xffffffffu, status != 0 || !alive)) {
+      cp_async_wait<0>();
+      break;
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  return status;
+}
+
+}  // namespace paqif

@@ -1,0 +1,128 @@
+"""Fused line-contact Newton step on the GPU vs teacher-forced reference
+steps (golden) and the numpy oracle.  Protocol SURVEY.md 8(c): single-step
+parity from identical states -- pressure and film within 1e-9 relative,
+identical cavitated set, identical solve rung (combined system vs the Ls4
+breakdown ladder) and force-balance application; plus a short horizon."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+G = load_golden("ehl_line.npz")
+KEYS = sorted({k.split("__")[0] for k in G.files if k.startswith("e")}, key=lambda s: int(s[1:]))
+TOL = 1e-9
+
+
+def gcase(key):
+    return {k.split("__", 1)[1]: G[k] for k in G.files if k.startswith(key + "__")}
+
+
+def params_for(d):
+    from paper_2008_03276_b200.ehl import EhlParams, moes_convert
+    m, l = float(d["meta"][0]), float(d["meta"][1])
+    u, w = moes_convert(m=m, l=l, g=5000.0)
+    p = EhlParams.line_from_loads(5000.0, u, w, domain=(-4.5, 1.5))
+    assert p.p_hertz == float(d["p_hertz"]) and p.lam == float(d["lam"])
+    return p
+
+
+def run_step(params_list, intervals, u_in, h0_in, k, exact=True):
+    from paper_2008_03276_b200.ehl import LineContactBatch
+    b = LineContactBatch(params_list, intervals, u0=u_in, h0=h0_in, exact=exact)
+    b.outer = k
+    b.step()
+    return b.snapshot()
+
+
+def check_against(d, u, h0, film, res, info):
+    ref = d["u_out"]
+    scale = max(1.0, float(np.max(np.abs(ref))))
+    assert np.max(np.abs(u - ref)) <= TOL * scale
+    assert np.array_equal(u == 0.0, ref == 0.0), "cavitated set differs"
+    assert math.isclose(h0, float(d["h0_out"]), rel_tol=1e-13, abs_tol=1e-15)
+    fref = d["film_out"]
+    assert np.max(np.abs(film - fref)) <= TOL * max(1.0, float(np.max(np.abs(fref))))
+    assert math.isclose(res, float(d["res_out"]), rel_tol=TOL)
+    assert ((info & 3) != 0) == (int(d["breaks"]) > 0), "solve rung differs"
+    assert bool(info & 4) == bool(d["fb_applied"])
+
+
+@pytest.mark.parametrize("key", KEYS)
+@pytest.mark.parametrize("exact", [True, False])
+def test_single_step_vs_reference(key, exact):
+    d = gcase(key)
+    p = params_for(d)
+    n, k = int(d["meta"][2]), int(d["meta"][3])
+    u, h0, film, res, _, info = run_step([p], n, d["u_in"][None], [float(d["h0_in"])], k, exact)
+    check_against(d, u[0], h0[0], film[0], res[0], int(info[0]))
+
+
+def test_batched_config3_cases_match_individually():
+    """All N=1025 golden states of one outer index in ONE launch."""
+    by_k = {}
+    for key in KEYS:
+        d = gcase(key)
+        if int(d["meta"][2]) == 1024:
+            by_k.setdefault(int(d["meta"][3]), []).append(d)
+    assert by_k
+    for k, ds in by_k.items():
+        ps = [params_for(d) for d in ds]
+        u0 = np.stack([d["u_in"] for d in ds])
+        h0 = [float(d["h0_in"]) for d in ds]
+        u, h0o, film, res, _, info = run_step(ps, 1024, u0, h0, k)
+        for j, d in enumerate(ds):
+            check_against(d, u[j], h0o[j], film[j], res[j], int(info[j]))
+
+
+def test_short_horizon_vs_oracle():
+    import oracle.ehl_oracle as E
+    from paper_2008_03276_b200.ehl import EhlParams, LineContactBatch, moes_convert
+    u_, w_ = moes_convert(m=20.0, l=10.0, g=5000.0)
+    p = EhlParams.line_from_loads(5000.0, u_, w_, domain=(-4.5, 1.5))
+    c = E.LineCase(p_hertz=p.p_hertz, lam=p.lam)
+    film = E.LineFilm(128, c)
+    ur, h0r = E.hertz_start(c, film), c.h0
+    b = LineContactBatch([p], 128)
+    for k in range(8):
+        ur, h0r, fr, rr, _ = E.line_step(ur, h0r, k, c, film)
+        b.step()
+        u, h0, f, res, _, _ = b.snapshot()
+        assert np.max(np.abs(u[0] - ur)) <= 1e-9 * max(1.0, np.max(np.abs(ur)))
+        assert math.isclose(res[0], rr, rel_tol=1e-8)
+        np.testing.assert_allclose(u[0], G["traj__u"][k], rtol=0, atol=1e-9)
+
+
+def test_line_deformation_matches_convolve(rng):
+    from paper_2008_03276_b200.ehl import kernel_line, line_deformation
+    n = 300
+    t = kernel_line(n, 0.02).table
+    u = np.abs(rng.standard_normal((3, n + 1)))
+    ext = np.concatenate([t[::-1], t[1:]])
+    ref = np.stack([-(1.0 / np.pi) * np.convolve(x, ext)[n:2 * n + 1] for x in u])
+    got = line_deformation(t, u)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_solve_ehl_line_api():
+    """solve_ehl runs the fused step; the reference never converges on config 1
+    (SURVEY.md 0.3), so a short budget raises NonConvergenceError with the
+    same residual history as the oracle's first iterations."""
+    import oracle.ehl_oracle as E
+    from paper_2008_03276_b200.errors import NonConvergenceError
+    from paper_2008_03276_b200.ehl import EhlParams, moes_convert, solve_ehl
+    u_, w_ = moes_convert(m=20.0, l=10.0, g=5000.0)
+    p = EhlParams.line_from_loads(5000.0, u_, w_, domain=(-4.5, 1.5))
+    seen = []
+    with pytest.raises(NonConvergenceError):
+        solve_ehl(p, 512, max_outer=6, collect=lambda st, r, d: seen.append(r))
+    c = E.LineCase(p_hertz=p.p_hertz, lam=p.lam)
+    film = E.LineFilm(512, c)
+    ur, h0r = E.hertz_start(c, film), c.h0
+    for k in range(3):
+        ur, h0r, _, rr, _ = E.line_step(ur, h0r, k, c, film)
+        assert math.isclose(seen[k], rr, rel_tol=1e-8)
