@@ -150,6 +150,89 @@ def cpu_reference_rate(bands, f, threads: int, min_core_seconds: float = 10.0):
     return reps * bands.shape[0] * N_ROWS / wall, wall, reps
 
 
+def _line_params(m, l):
+    from paper_2008_03276_b200.ehl import EhlParams, moes_convert
+    u, w = moes_convert(m=m, l=l, g=5000.0)
+    return EhlParams.line_from_loads(5000.0, u, w, domain=(-4.5, 1.5))
+
+
+def config3_cases(rank, count=1024, seed=SEED):
+    """Config 3 load sweep: M log-uniform on [5, 200], L uniform on [5, 15];
+    case c drawn from default_rng((seed, 3, c)) so shards are rank-invariant."""
+    import numpy as np
+    out = []
+    for c in range(rank * count, (rank + 1) * count):
+        g = np.random.default_rng((seed, 3, c))
+        m = float(np.exp(g.uniform(np.log(5.0), np.log(200.0))))
+        out.append((m, float(g.uniform(5.0, 15.0))))
+    return out
+
+
+def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5):
+    """EHL Newton-step throughput: config 1 (one line contact, N=513) and
+    config 3 (1024 line contacts per GPU, N=1025), device-timed per outer
+    iteration, plus the oracle CPU rate on this host."""
+    import numpy as np
+    import torch
+    from paper_2008_03276_b200.ehl import LineContactBatch
+    out = {}
+    stream = torch.cuda.current_stream()
+
+    def timed(batch, k):
+        for _ in range(3):
+            batch.step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            batch.step()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / k
+
+    p1 = _line_params(20.0, 10.0)
+    ms1 = timed(LineContactBatch([p1], 512), steps1)
+    out["config1"] = {"metric": "EHL Newton iters/s (line, N=513, M=20, L=10, B=1)",
+                      "value": 1e3 / ms1, "unit": "iters/s", "us_per_iter": ms1 * 1e3,
+                      "gpu_launches_per_iter": 1}
+    cases = config3_cases(rank)
+    b3 = LineContactBatch([_line_params(m, l) for m, l in cases], 1024)
+    ms3 = timed(b3, steps3)
+    info = b3.info.cpu().numpy()
+    out["config3"] = {"metric": "EHL line-contact case-iterations/s (1024 cases/GPU, N=1025)",
+                      "value": world * len(cases) * 1e3 / ms3, "unit": "case-iters/s",
+                      "ms_per_iter": ms3, "scaling": "weak",
+                      "ladder_cases_last_iter": int(np.sum((info & 3) > 0))}
+    if with_cpu:
+        import oracle.ehl_oracle as E
+        c = E.LineCase(p_hertz=p1.p_hertz, lam=p1.lam)
+        f = E.LineFilm(512, c)
+        u, h0 = E.hertz_start(c, f), c.h0
+        t0 = time.perf_counter()
+        k = 0
+        while k < 20 or time.perf_counter() - t0 < 3.0:
+            u, h0, _, _, _ = E.line_step(u, h0, k, c, f)
+            k += 1
+        dt = (time.perf_counter() - t0) / k
+        out["config1"]["cpu_baseline"] = {"value": 1.0 / dt, "unit": "iters/s", "cores": 1,
+                                          "kind": "port",
+                                          "sample": f"{k} oracle line steps (numpy restatement)"}
+        c3 = E.LineCase(p_hertz=b3.p_hertz[0].item(), lam=b3.lam[0].item())
+        f3 = E.LineFilm(1024, c3)
+        u3, h3 = E.hertz_start(c3, f3), c3.h0
+        t0 = time.perf_counter()
+        k = 0
+        while k < 5 or time.perf_counter() - t0 < 3.0:
+            u3, h3, _, _, _ = E.line_step(u3, h3, k, c3, f3)
+            k += 1
+        dt3 = (time.perf_counter() - t0) / k
+        out["config3"]["cpu_baseline"] = {"value": 1.0 / dt3, "unit": "case-iters/s",
+                                          "cores": 1, "kind": "port",
+                                          "sample": f"{k} oracle steps of case 0, one core"}
+    return out
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU implementation of the path
     (oracle port, all host threads), rank 0 only."""
@@ -193,6 +276,7 @@ def main():
     ap.add_argument("--fast", action="store_true", help="FMA arithmetic (default: exact)")
     ap.add_argument("--batch", type=int, default=B_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ehl", action="store_true", help="skip the config-1/3 EHL lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -323,6 +407,9 @@ def main():
                  "peak_src": "tools/peaks.cu DFMA microbenchmark (profiles/peaks_r01.json)"},
         "clocks": clocks.summary(),
     }
+    if not args.no_ehl:
+        line["secondary"] = ehl_secondary(rank, world, with_cpu=(rank == 0 and world == 1
+                                                                  and not args.no_cpu_baseline))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
         sample = 1024
