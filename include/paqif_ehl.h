@@ -62,6 +62,58 @@ int paqif_line_deformation(int64_t B, int64_t n, const double *table /*[dev] n+1
                            const double *u /*[dev] (B, n+1)*/, double *out /*[dev] (B, n+1)*/,
                            void *stream);
 
+/* ------------------------------------------------------------ point contact
+ * One outer iteration of ehl.solver.solve_ehl for the circular point contact
+ * (configs 4/5) on an (n+1)^2 grid, in the reference's Gauss-Seidel order:
+ *   _hybrid_x_sweep (ehl/solver.py:76-128; per-row Newton Ls1 or weighted Ls4
+ *   by min(eps)/h > 0.6), column_sweep (ehl/sweeps.py:421-518),
+ *   force_balance_update (ehl/sweeps.py:521-535, weight h^2) and
+ *   complementarity_residual (ehl/solver.py:43-51).
+ * The deformation is FilmModel('point') (ehl/film.py:43-155): fp64 FFT
+ * convolution plus exact pending-line corrections, folded after > 8 pending
+ * updates.  The handle owns all device state (one CUDA stream, HBM resident
+ * pressure / deformation / film fields); a native host loop drives the
+ * 2(n-1) line kernels. */
+typedef struct {
+  int32_t n;            /* grid intervals per axis                            */
+  int32_t limiter;      /* 0 kappa, 1 none, 2 van-albada, 3 minmod, 4 koren   */
+  int32_t variant;      /* 0 Lhs1 (Ls1/Ls4), 1 Lhs2 (Ls0/Ls5)                 */
+  int32_t compressible; /* Dowson-Higginson + Roelands (1) or unit (0)        */
+  int32_t force_every;  /* force-balance period                               */
+  int32_t outer;        /* ignored in the cfg; passed to _step                */
+  double h;             /* spacing (both axes)                                */
+  double kappa, omega, max_change, relax_c, max_h0_step, load_target;
+  double alpha, z, p0;  /* pressure-viscosity constants                       */
+  double p_hertz, lam;  /* case constants (EhlParams.point_from_moes)          */
+} paqif_ehl_point_cfg;
+
+typedef struct paqif_ehl_point paqif_ehl_point;
+
+/* Creates the solver state; table (kernels.kernel_point) and geometry
+ * (0.5 (x^2 + y^2)) are HOST (n+1)^2 row-major arrays [j][i].  NULL on error
+ * (paqif_last_error). */
+paqif_ehl_point *paqif_ehl_point_create(const paqif_ehl_point_cfg *cfg, const double *table,
+                                        const double *geometry);
+void paqif_ehl_point_destroy(paqif_ehl_point *h);
+
+/* Loads pressure u (HOST (n+1)^2) and offset h0; recomputes the deformation. */
+int paqif_ehl_point_set_state(paqif_ehl_point *h, const double *u, double h0);
+
+/* Enqueues one outer iteration (asynchronous on the handle's stream). */
+int paqif_ehl_point_step(paqif_ehl_point *h, int32_t outer, uint32_t flags);
+
+/* Synchronises and copies results to HOST buffers (any may be NULL):
+ *   u, film (n+1)^2;  scal[3] = {h0, complementarity residual, deficit};
+ *   xinfo (n-1): bit 0 Newton line, bits 4..5 ladder rung (3 = failed);
+ *   yinfo (n-1): rung (0 tridiagonal, 1 diagonal, 3 failed);
+ *   err: bit 0/2 an x/y line broke down on every rung, 1/3 non-finite change */
+int paqif_ehl_point_get(paqif_ehl_point *h, double *u, double *film, double *scal,
+                        int32_t *xinfo, int32_t *yinfo, int32_t *err);
+int paqif_ehl_point_sync(paqif_ehl_point *h);
+
+/* Deformation of HOST pressure u into HOST out (FilmModel.deformation_full). */
+int paqif_ehl_point_deformation(paqif_ehl_point *h, const double *u, double *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,755 @@
+// EHL point contact (configs 4/5): one outer iteration of solve_ehl in the
+// reference's Gauss-Seidel order (paqif/ehl/solver.py:76-128 then
+// ehl/sweeps.py:421-518), driven by a native host loop over the grid lines.
+//
+// Device state mirrors FilmModel's bookkeeping (ehl/film.py:83-155): the
+// deformation base of the last full evaluation plus up to 9 pending line
+// updates whose exact contribution is added to the few film rows/columns a
+// line needs; a fold (full FFT deformation, fft_deform.cuh) runs as soon as
+// more than 8 are pending, decided on the device (gated kernels).
+//
+// Per line: pt_films (multi-CTA: base + pending corrections for the 3
+// rows / <=4 columns the line reads) -> pt_xline / pt_yline (one CTA:
+// rheology, limited faces, residual, assembly with the bad-row fix, AQIF
+// line solve on warp 0 with the reference's fallback ladder, clip, immediate
+// update or deferred weighted change, pending note) -> gated fold.
+#include <cfloat>
+#include <vector>
+#include "ehl_common.cuh"
+#include "ehl_solve.cuh"
+#include "fft_deform.cuh"
+#include "capi_util.cuh"
+
+extern "C" {
+#include "../../include/paqif_ehl.h"
+}
+
+namespace paqif {
+
+constexpr int kPtThreads = 256;
+constexpr int kMaxPending = 9;
+enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMSize = 24 };
+
+struct PointDev {
+  int n, N, n_sys;
+  double* u;
+  double* geom;
+  double* table;
+  double* dbase;
+  double* films;    // 4 x N
+  double* sigma;    // N x N
+  double* pend;     // kMaxPending x N
+  int* meta;        // kMSize ints
+  double* scal;     // [0] h0, [1] res, [2] deficit, [3] comp max bits
+  double* scratch;  // line solve scratch
+  int32_t* xinfo;   // n-1: newton tag | rung << 4
+  int32_t* yinfo;   // n-1: rung
+  double* film_out; // N x N
+};
+
+__device__ __forceinline__ double rheo_eps(double u, double film, const paqif_ehl_point_cfg& c,
+                                           double& rho) {
+  double eta;
+  if (c.compressible) {
+    const double p = u * c.p_hertz;
+    rho = (kDensA + kDensB * p) / (kDensA + p);
+    const double arg = (c.alpha * c.p0 / c.z) * (-1.0 + pow(1.0 + p / c.p0, c.z));
+    eta = exp(np_minimum(arg, 200.0));
+  } else {
+    rho = 1.0;
+    eta = 1.0;
+  }
+  const double coeff = rho / (eta * c.lam);
+  const double gap = np_maximum(film, 1e-8);
+  return coeff * (gap * gap * gap);
+}
+
+// films of `L` consecutive rows (mode 0) or columns (mode 1) starting at `first`
+__global__ void pt_films_kernel(PointDev d, int mode, int first, int L) {
+  const int N = d.N;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (idx >= N || l >= L) return;
+  const int line = first + l;
+  const double h0 = d.scal[0];
+  const int count = d.meta[kMCount];
+  const size_t g = mode == 0 ? (size_t)line * N + idx : (size_t)idx * N + line;
+  double v = (h0 + d.geom[g]) + d.dbase[g];
+  if (count > 0) {
+    double corr = 0.0;
+    for (int p = 0; p < count; ++p) {
+      const int axis = d.meta[kMAxis + p], ell = d.meta[kMIdx + p];
+      const double* delta = d.pend + (size_t)p * N;
+      double s = 0.0;
+      if (axis == mode) {
+        // same axis: 1-D Toeplitz convolution with the kernel row |line-ell|
+        const double* tr = d.table + (size_t)abs(line - ell) * N;
+        for (int k = 0; k < N; ++k) s = fma(tr[abs(idx - k)], delta[k], s);
+      } else {
+        // cross axis: gather-matvec (film.py:114-117, 131-134; symmetric table)
+        const double* tr = d.table + (size_t)abs(idx - ell) * N;
+        for (int k = 0; k < N; ++k) s = fma(tr[abs(line - k)], delta[k], s);
+      }
+      corr += s;
+    }
+    v = v + corr;
+  }
+  d.films[(size_t)l * N + idx] = v;
+}
+
+__device__ __forceinline__ double block_min(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmin(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+// assemble_line_system row for an x-line of the point contact (hy = h,
+// ey terms, bad-row fix; sweeps.py:157-267).  jac: 0 scheme, 1 first-order,
+// 2 diagonal.  ex/ey already carry the factor h (sweeps.py:329-334).
+__device__ __forceinline__ void point_row(double rw, double rc, double re, double ex_p,
+                                          double ex_m, double ey_p, double ey_m, double phi_p,
+                                          double phi_m, double h, bool weighted, int jac,
+                                          double ks0, double ks1, double* e) {
+  if (jac != 0) {
+    phi_p = 0.0;
+    phi_m = 0.0;
+  }
+  const double a_p = 1.0 - 0.5 * phi_p, b_p = 0.5 * phi_p;
+  const double a_m = 1.0 - 0.5 * phi_m, b_m = 0.5 * phi_m;
+  const double hy = h;
+  double c_m2, c_m1, c_0, c_p1, c_p2;
+  if (jac == 2) {
+    c_m2 = 0.0; c_m1 = 0.0; c_p1 = 0.0; c_p2 = 0.0;
+    c_0 = -hy * rc * fabs(ks0);
+  } else {
+    c_m2 = hy * (a_m * rw * ks1);
+    c_m1 = -hy * (a_p * rc * ks1 - a_m * rw * ks0 - b_m * rc * ks1);
+    c_0 = -hy * (a_p * rc * ks0 + b_p * re * ks1 - a_m * rw * ks1 - b_m * rc * ks0);
+    c_p1 = -hy * (a_p * rc * ks1 + b_p * re * ks0 - b_m * rc * ks1);
+    c_p2 = -hy * (b_p * re * ks1);
+  }
+  const double ey_sum = ey_p + ey_m;
+  double p_m2, p_m1, p_0, p_p1, p_p2;
+  if (weighted) {
+    p_m2 = -0.25 * ex_m / h;
+    p_m1 = (1.25 * ex_m + 0.25 * ex_p) / h + 0.25 * ey_sum / h;
+    p_0 = -1.25 * (ex_p + ex_m + ey_sum) / h;
+    p_p1 = (1.25 * ex_p + 0.25 * ex_m) / h + 0.25 * ey_sum / h;
+    p_p2 = -0.25 * ex_p / h;
+  } else {
+    p_m2 = 0.0;
+    p_m1 = ex_m / h;
+    p_0 = -(ex_p + ex_m + ey_sum) / h;
+    p_p1 = ex_p / h;
+    p_p2 = 0.0;
+  }
+  e[0] = -(c_m2 + p_m2);
+  e[1] = -(c_m1 + p_m1);
+  e[2] = -(c_0 + p_0);
+  e[3] = -(c_p1 + p_p1);
+  e[4] = -(c_p2 + p_p2);
+  const double off_mag = fabs(e[0]) + fabs(e[1]) + fabs(e[3]) + fabs(e[4]);
+  const double floor_ = 0.05 * hy * fabs(rc) * fabs(ks0);
+  if (fabs(e[2]) < np_maximum(0.2 * off_mag, floor_)) {
+    const double fo_m2 = hy * rw * ks1;
+    const double fo_m1 = -hy * (rc * ks1 - rw * ks0);
+    const double fo_0 = -hy * (rc * ks0 - rw * ks1);
+    const double fo_p1 = -hy * rc * ks1;
+    e[0] = -(fo_m2 + p_m2);
+    e[1] = -(fo_m1 + p_m1);
+    e[2] = -(fo_0 + p_0);
+    e[3] = -(fo_p1 + p_p1);
+    e[4] = -p_p2;
+  }
+}
+
+struct PtShared {
+  double red[32];
+  int flag;
+  int any;
+  int pad[2];
+};
+
+// write one assembled row (padded-matrix semantics) of the line system
+__device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, int n_int, int r,
+                                        const double* e, double rr) {
+#pragma unroll
+  for (int dd = 0; dd < 5; ++dd) {
+    const int col = r + dd - kLineBeta;
+    const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (dd == kLineBeta);
+    band[(size_t)dd * n_sys + r] = keep ? e[dd] : 0.0;
+  }
+  rhs[r] = rr;
+}
+
+// x-line j of _hybrid_x_sweep (solver.py:91-114) with _line_quantities
+// (sweeps.py:318-341) and assemble_line_system's point terms (sweeps.py:157-267)
+template <bool EXACT>
+__global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
+                                                              int j) {
+  extern __shared__ __align__(16) double xsm[];
+  PtShared& S = *reinterpret_cast<PtShared*>(xsm);
+  EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(xsm + sizeof(PtShared) / 8);
+  double* ring = xsm + sizeof(PtShared) / 8 + sizeof(EngineSmem<kLineBeta>) / 8;
+  const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
+  const double h = c.h;
+  const double* u = d.u;
+  const double* F = d.films;  // rows j-1, j, j+1
+  auto film = [&](int r, int i) { return F[(size_t)(r - (j - 1)) * N + i]; };
+  auto eps_at = [&](int r, int i, double& rho) {
+    return rheo_eps(u[(size_t)r * N + i], film(r, i), c, rho);
+  };
+  // pass 1: min(eps_line)/h and max|q_line|
+  double emin = INFINITY, qmax = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double rho;
+    const double e = eps_at(j, i, rho);
+    emin = fmin(emin, e);
+    qmax = fmax(qmax, fabs(rho * film(j, i)));
+  }
+  const double ratio = block_min(emin, S.red) / h;
+  const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
+  const bool newton = ratio > kSwitch;
+  const bool weighted = !newton;
+  // kernel sensitivities (film.sensitivity, point: table[|d|][|off|])
+  const double* t = d.table;
+  const double s00 = t[0], s10 = t[N], s20 = t[2 * N], s01 = t[1], s11 = t[N + 1];
+  const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
+                                   : (2.0 - c.kappa) / 2.0 + (1.0 - c.kappa) / 4.0;
+  double ks0, ks1;
+  if (weighted) {
+    ks0 = nu * (s00 - 0.25 * (2.0 * s10 + 2.0 * s01));
+    ks1 = nu * (s10 - 0.25 * (s00 + s20 + 2.0 * s11));
+  } else {
+    ks0 = s00;
+    ks1 = s10;
+  }
+  double* band = d.scratch;
+  double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
+  int rung = 0;
+  int st = 1;
+  for (; rung < 3; ++rung) {
+    for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
+      double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
+      double rr = 0.0;
+      if (r < n_int) {
+        const int i = r + 1;
+        double rw, rc, re, rdum, rm2 = 0.0;
+        const double ew = eps_at(j, i - 1, rw);
+        const double ec = eps_at(j, i, rc);
+        const double ee = eps_at(j, i + 1, re);
+        const double es = eps_at(j - 1, i, rdum);
+        const double en = eps_at(j + 1, i, rdum);
+        const double qw = rw * film(j, i - 1), qc = rc * film(j, i), qe = re * film(j, i + 1);
+        double qww = 0.0;
+        if (i >= 2) {
+          eps_at(j, i - 2, rm2);
+          qww = rm2 * film(j, i - 2);
+        }
+        const double dqi = qe - qc, dqm = qc - qw;
+        const double php = limiter_wplus(gratio(dqi, dqm, gfloor), c.limiter, c.kappa);
+        const double phm = i >= 2 ? limiter_wplus(gratio(dqm, qw - qww, gfloor), c.limiter, c.kappa)
+                                  : 0.0;
+        const double fd = (qc + 0.5 * php * dqi) - (qw + 0.5 * phm * dqm);
+        const double ex_p = 0.5 * (ec + ee) * h, ex_m = 0.5 * (ec + ew) * h;
+        const double ey_p = 0.5 * (ec + en) * h, ey_m = 0.5 * (ec + es) * h;
+        const double uc = u[(size_t)j * N + i];
+        rr = (ex_p * (u[(size_t)j * N + i + 1] - uc) + ex_m * (u[(size_t)j * N + i - 1] - uc)) / h +
+             (ey_p * (u[(size_t)(j + 1) * N + i] - uc) + ey_m * (u[(size_t)(j - 1) * N + i] - uc)) / h -
+             h * fd;
+        point_row(rw, rc, re, ex_p, ex_m, ey_p, ey_m, php, phm, h, weighted, rung, ks0, ks1, e);
+      }
+      put_row(band, rhs, n_sys, n_int, r, e, rr);
+    }
+    st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
+    if (!st) break;
+  }
+  if (st) {
+    if (threadIdx.x == 0) {
+      atomicOr(&d.meta[kMErr], 1);
+      d.xinfo[j - 1] = (newton ? 1 : 0) | (3 << 4);
+    }
+    return;
+  }
+  const double* x = line_solution(d.scratch, n_sys);
+  int nz = 0, fin = 1;
+  double* delta = d.pend + (size_t)d.meta[kMCount] * N;  // next pending slot (used if newton)
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    if (i >= 1 && i <= n - 1) {
+      double sg = x[i - 1];
+      fin &= isfinite(sg);
+      sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
+      if (newton) {
+        const double old = u[(size_t)j * N + i];
+        const double nv = np_maximum(0.0, old + c.omega * sg);
+        const double dl = nv - old;
+        nz |= (dl != 0.0) || (dl != dl);
+        delta[i] = dl;
+        d.u[(size_t)j * N + i] = nv;
+      } else {
+        d.sigma[(size_t)j * N + i] = sg;
+      }
+    } else if (newton) {
+      delta[i] = 0.0;
+    }
+  }
+  nz = __syncthreads_or(nz);
+  fin = __syncthreads_and(fin);
+  if (threadIdx.x == 0) {
+    if (!fin) atomicOr(&d.meta[kMErr], 2);
+    d.xinfo[j - 1] = (newton ? 1 : 0) | (rung << 4);
+    if (newton && nz) {  // note_line_update("row", j, delta, u)
+      const int p = d.meta[kMCount];
+      d.meta[kMAxis + p] = 0;
+      d.meta[kMIdx + p] = j;
+      d.meta[kMCount] = p + 1;
+      if (p + 1 > 8) d.meta[kMGate] = 1;
+    }
+    if (weighted) d.meta[kMAnyW] = 1;
+  }
+}
+
+// deferred weighted changes of the x-sweep (solver.py:115-127)
+__global__ void pt_weighted_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  if (d.meta[kMAnyW] == 0) return;
+  const int N = d.N, n = d.n;
+  const size_t total = (size_t)N * N;
+  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(g / N), i = (int)(g % N);
+    const double* s = d.sigma;
+    double sp = 0.0;
+    if (i >= 1) sp += s[g - 1];
+    if (i < n) sp += s[g + 1];
+    if (j >= 1) sp += s[g - N];
+    if (j < n) sp += s[g + N];
+    double v = np_maximum(0.0, d.u[g] + c.omega * (s[g] - 0.25 * sp));
+    if (i == 0 || i == n || j == 0 || j == n) v = 0.0;
+    d.film_out[g] = v;  // staged: u must not change while neighbours are read
+  }
+}
+__global__ void pt_copy_kernel(double* dst, const double* src, size_t count, const int* flag) {
+  if (flag && *flag == 0) return;
+  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < count;
+       g += (size_t)gridDim.x * blockDim.x)
+    dst[g] = src[g];
+}
+__global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (!from_anyw || meta[kMAnyW]) meta[kMGate] = 1;
+  }
+}
+
+// column i of column_sweep (sweeps.py:437-517)
+template <bool EXACT>
+__global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
+                                                              int i) {
+  extern __shared__ __align__(16) double ysm[];
+  PtShared& S = *reinterpret_cast<PtShared*>(ysm);
+  EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(ysm + sizeof(PtShared) / 8);
+  double* ring = ysm + sizeof(PtShared) / 8 + sizeof(EngineSmem<kLineBeta>) / 8;
+  const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
+  const double h = c.h;
+  const int lo = i - 2 > 0 ? i - 2 : 0;
+  const int L = i + 2 - lo, pos = i - lo;
+  const double* u = d.u;
+  const double* F = d.films;  // columns lo..i+1, indexed [l][m]
+  auto film = [&](int l, int m) { return F[(size_t)l * N + m]; };
+  auto eps_at = [&](int l, int m, double& rho) {
+    return rheo_eps(u[(size_t)m * N + (lo + l)], film(l, m), c, rho);
+  };
+  double qmax = 0.0;
+  for (int k = threadIdx.x; k < L * N; k += blockDim.x) {
+    const int l = k / N, m = k % N;
+    double rho;
+    eps_at(l, m, rho);
+    qmax = fmax(qmax, fabs(rho * film(l, m)));
+  }
+  const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
+  const double* t = d.table;
+  const double s00 = t[0], s10 = t[N], s01 = t[1], s11 = t[N + 1];
+  double* band = d.scratch;
+  double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
+  int st = 1, rung = 0;
+  for (; rung < 2; ++rung) {  // 0: tridiagonal system, 1: diagonal fallback
+    for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
+      double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
+      double rr = 0.0;
+      if (r < n_int) {
+        const int jj = r + 1;
+        double rc, rw, re, rdum, rww = 0.0;
+        const double ec = eps_at(pos, jj, rc);
+        const double ew = eps_at(pos - 1, jj, rw);
+        const double ee = eps_at(pos + 1, jj, re);
+        const double es = eps_at(pos, jj - 1, rdum);
+        const double en = eps_at(pos, jj + 1, rdum);
+        const double ey_p = 0.5 * (ec + en) * h, ey_m = 0.5 * (ec + es) * h;
+        const double ex_p = 0.5 * (ec + ee) * h, ex_m = 0.5 * (ec + ew) * h;
+        const double qc = rc * film(pos, jj), qw = rw * film(pos - 1, jj), qe = re * film(pos + 1, jj);
+        const double dq_p = qe - qc, dq_m = qc - qw;
+        const double php = limiter_wplus(gratio(dq_p, dq_m, gfloor), c.limiter, c.kappa);
+        double phm = 0.0;
+        if (pos >= 2) {
+          eps_at(pos - 2, jj, rww);
+          const double qww = rww * film(pos - 2, jj);
+          phm = limiter_wplus(gratio(dq_m, qw - qww, gfloor), c.limiter, c.kappa);
+        }
+        const double flux_p = qc + 0.5 * php * dq_p;
+        const double flux_m = qw + 0.5 * phm * dq_m;
+        const double uc = u[(size_t)jj * N + i];
+        rr = (ex_p * (u[(size_t)jj * N + i + 1] - uc) + ex_m * (u[(size_t)jj * N + i - 1] - uc)) / h +
+             (ey_p * (u[(size_t)(jj + 1) * N + i] - uc) + ey_m * (u[(size_t)(jj - 1) * N + i] - uc)) / h -
+             h * (flux_p - flux_m);
+        if (rung == 0) {
+          const double a_p = 1.0 - 0.5 * php, b_p = 0.5 * php;
+          const double a_m = 1.0 - 0.5 * phm, b_m = 0.5 * phm;
+          double c_diag = -h * ((a_p - b_m) * rc * s00 + (b_p * re - a_m * rw) * s10);
+          double c_off = -h * ((a_p - b_m) * rc * s01 + (b_p * re - a_m * rw) * s11);
+          double diag_full = -(ey_p + ey_m + ex_p + ex_m) / h + c_diag;
+          const double floor_ = 0.05 * h * fabs(rc) * s00;
+          if (fabs(diag_full) < floor_) {
+            c_diag = -h * (rc * s00 - rw * s10);
+            c_off = -h * (rc * s01 - rw * s11);
+            diag_full = -(ey_p + ey_m + ex_p + ex_m) / h + c_diag;
+          }
+          e[0] = 0.0;
+          e[1] = -(ey_m / h + c_off);
+          e[2] = -diag_full;
+          e[3] = -(ey_p / h + c_off);
+          e[4] = 0.0;
+        } else {
+          e[0] = 0.0; e[1] = 0.0; e[3] = 0.0; e[4] = 0.0;
+          e[2] = (ey_p + ey_m + ex_p + ex_m) / h + h * fabs(rc) * s00;
+        }
+      }
+      put_row(band, rhs, n_sys, n_int, r, e, rr);
+    }
+    st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
+    if (!st) break;
+  }
+  if (st) {
+    if (threadIdx.x == 0) {
+      atomicOr(&d.meta[kMErr], 4);
+      d.yinfo[i - 1] = 3;
+    }
+    return;
+  }
+  const double* x = line_solution(d.scratch, n_sys);
+  int nz = 0, fin = 1;
+  double* delta = d.pend + (size_t)d.meta[kMCount] * N;
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    if (m >= 1 && m <= n - 1) {
+      double sg = x[m - 1];
+      fin &= isfinite(sg);
+      sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
+      const double old = u[(size_t)m * N + i];
+      const double nv = np_maximum(0.0, old + c.omega * sg);
+      const double dl = nv - old;
+      nz |= (dl != 0.0) || (dl != dl);
+      delta[m] = dl;
+      d.u[(size_t)m * N + i] = nv;
+    } else {
+      delta[m] = 0.0;
+    }
+  }
+  nz = __syncthreads_or(nz);
+  fin = __syncthreads_and(fin);
+  if (threadIdx.x == 0) {
+    if (!fin) atomicOr(&d.meta[kMErr], 8);
+    d.yinfo[i - 1] = rung;
+    if (nz) {  // note_line_update("col", i, delta, u)
+      const int p = d.meta[kMCount];
+      d.meta[kMAxis + p] = 1;
+      d.meta[kMIdx + p] = i;
+      d.meta[kMCount] = p + 1;
+      if (p + 1 > 8) d.meta[kMGate] = 1;
+    }
+  }
+}
+
+// force balance (sweeps.py:521-535, weight h^2)
+__global__ void pt_force_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  __shared__ double red[32];
+  const size_t total = (size_t)d.N * d.N;
+  double part = 0.0;
+  for (size_t g = threadIdx.x; g < total; g += blockDim.x) part += d.u[g];
+  const double sum = block_sum(part, red);
+  if (threadIdx.x == 0) {
+    const double deficit = c.load_target - (c.h * c.h) * sum;
+    const double stp = np_minimum(np_maximum(c.relax_c * deficit, -c.max_h0_step), c.max_h0_step);
+    d.scal[0] = d.scal[0] - stp;
+    d.scal[2] = deficit;
+  }
+}
+
+// reynolds_residual_field (2-D, sweeps.py:124-140) and the complementarity
+// residual; one CTA per row; film_out = h0 + geometry + deformation
+__global__ void pt_residual_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  __shared__ double red[32];
+  const int n = d.n, N = d.N;
+  const int j = blockIdx.x;
+  const double h = c.h, h0 = d.scal[0];
+  auto film = [&](int r, int i) { return (h0 + d.geom[(size_t)r * N + i]) + d.dbase[(size_t)r * N + i]; };
+  auto eps_at = [&](int r, int i, double& rho) {
+    return rheo_eps(d.u[(size_t)r * N + i], film(r, i), c, rho);
+  };
+  for (int i = threadIdx.x; i < N; i += blockDim.x) d.film_out[(size_t)j * N + i] = film(j, i);
+  double comp = 0.0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (j >= 1 && j <= n - 1) {
+    double qmax = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      double rho;
+      eps_at(j, i, rho);
+      qmax = fmax(qmax, fabs(rho * film(j, i)));
+    }
+    const double gfloor = 1e-12 * fmax(block_max(qmax, red), kRatioGuard);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      double r = 0.0;
+      if (i >= 1 && i <= n - 1) {
+        double rw, rc, re, rdum, rww = 0.0;
+        const double ew = eps_at(j, i - 1, rw);
+        const double ec = eps_at(j, i, rc);
+        const double ee = eps_at(j, i + 1, re);
+        const double es = eps_at(j - 1, i, rdum);
+        const double en = eps_at(j + 1, i, rdum);
+        const double qw = rw * film(j, i - 1), qc = rc * film(j, i), qe = re * film(j, i + 1);
+        const double dqi = qe - qc, dqm = qc - qw;
+        const double php = limiter_wplus(gratio(dqi, dqm, gfloor), c.limiter, c.kappa);
+        double phm = 0.0;
+        if (i >= 2) {
+          eps_at(j, i - 2, rww);
+          phm = limiter_wplus(gratio(dqm, qw - rww * film(j, i - 2), gfloor), c.limiter, c.kappa);
+        }
+        const double fd = (qc + 0.5 * php * dqi) - (qw + 0.5 * phm * dqm);
+        const double exp_ = 0.5 * (ec + ee) * h, exm = 0.5 * (ec + ew) * h;
+        const double eyp = 0.5 * (ec + en) * h, eym = 0.5 * (ec + es) * h;
+        const double uc = d.u[(size_t)j * N + i];
+        r = (exp_ * (d.u[(size_t)j * N + i + 1] - uc) + exm * (d.u[(size_t)j * N + i - 1] - uc)) / h +
+            (eyp * (d.u[(size_t)(j + 1) * N + i] - uc) + eym * (d.u[(size_t)(j - 1) * N + i] - uc)) / h -
+            h * fd;
+      }
+      const double m = fabs(np_minimum(d.u[(size_t)j * N + i], -r));
+      comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+    }
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double m = fabs(np_minimum(d.u[(size_t)j * N + i], -0.0));
+      comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+    }
+  }
+  const double cm = block_nanmax(comp, red);
+  if (threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&d.scal[3]),
+              (unsigned long long)__double_as_longlong(cm));
+}
+
+__global__ void pt_finish_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) d.scal[1] = d.scal[3] / (c.h * c.h);
+}
+
+}  // namespace paqif
+
+using namespace paqif;
+
+// ============================================================== native driver
+struct paqif_ehl_point {
+  paqif_ehl_point_cfg cfg;
+  PointDev d;
+  FftPlan plan;
+  cudaStream_t st;
+  std::vector<void*> allocs;
+  size_t line_smem;
+};
+
+namespace {
+
+template <class T>
+T* dalloc(paqif_ehl_point* h, size_t count) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+  h->allocs.push_back(p);
+  cudaMemsetAsync(p, 0, count * sizeof(T), h->st);
+  return (T*)p;
+}
+
+void fold(paqif_ehl_point* h) {
+  fft_deformation(h->plan, h->d.u, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount], h->st);
+}
+
+}  // namespace
+
+extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cfg,
+                                                   const double* table, const double* geometry) {
+  if (!cfg || cfg->n < 8 || cfg->n > 8192) {
+    set_arg_error("ehl_point: bad cfg");
+    return nullptr;
+  }
+  auto* h = new paqif_ehl_point();
+  h->cfg = *cfg;
+  if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return nullptr;
+  }
+  const int n = cfg->n, N = n + 1, n_int = n - 1;
+  const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+  PointDev& d = h->d;
+  d.n = n;
+  d.N = N;
+  d.n_sys = n_sys;
+  const size_t NN = (size_t)N * N;
+  d.u = dalloc<double>(h, NN);
+  d.geom = dalloc<double>(h, NN);
+  d.table = dalloc<double>(h, NN);
+  d.dbase = dalloc<double>(h, NN);
+  d.films = dalloc<double>(h, 4 * (size_t)N);
+  d.sigma = dalloc<double>(h, NN);
+  d.pend = dalloc<double>(h, (size_t)kMaxPending * N);
+  d.meta = dalloc<int>(h, kMSize);
+  d.scal = dalloc<double>(h, 8);
+  d.scratch = dalloc<double>(h, line_scratch_doubles(n_sys));
+  d.xinfo = dalloc<int32_t>(h, N);
+  d.yinfo = dalloc<int32_t>(h, N);
+  d.film_out = dalloc<double>(h, NN);
+  FftPlan& p = h->plan;
+  p.n = n;
+  p.P = fft_size_for(n);
+  p.logP = 0;
+  while ((1 << p.logP) < p.P) ++p.logP;
+  const size_t PP = (size_t)p.P * p.P;
+  p.W = dalloc<double2>(h, PP);
+  p.T = dalloc<double2>(h, PP);
+  p.KT = dalloc<double2>(h, PP);
+  p.tw = dalloc<double2>(h, p.P / 2 + 1);
+  for (void* a : h->allocs)
+    if (!a) {
+      paqif_ehl_point_destroy(h);
+      set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
+      return nullptr;
+    }
+  if (h->allocs.size() != 17) {
+    paqif_ehl_point_destroy(h);
+    set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
+    return nullptr;
+  }
+  cudaMemcpyAsync(d.table, table, NN * 8, cudaMemcpyHostToDevice, h->st);
+  cudaMemcpyAsync(d.geom, geometry, NN * 8, cudaMemcpyHostToDevice, h->st);
+  fft_prepare(p.P);
+  fft_plan_kernel(p, d.table, h->st);
+  h->line_smem = sizeof(PtShared) + sizeof(EngineSmem<kLineBeta>) +
+                 ZChunk<kLineBeta>::kRing * sizeof(double);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess || check_launch("ehl_point_create")) {
+    paqif_ehl_point_destroy(h);
+    return nullptr;
+  }
+  return h;
+}
+
+extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
+  if (!h) return;
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (void* a : h->allocs)
+    if (a) cudaFree(a);
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+extern "C" int paqif_ehl_point_set_state(paqif_ehl_point* h, const double* u, double h0) {
+  if (!h || !u) return set_arg_error("ehl_point_set_state");
+  const size_t NN = (size_t)h->d.N * h->d.N;
+  cudaMemcpyAsync(h->d.u, u, NN * 8, cudaMemcpyHostToDevice, h->st);
+  double s[8] = {h0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyAsync(h->d.scal, s, sizeof(s), cudaMemcpyHostToDevice, h->st);
+  cudaMemsetAsync(h->d.meta, 0, kMSize * sizeof(int), h->st);
+  pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
+  fold(h);  // deformation_full(u): fresh base, no pending updates
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? check_launch("ehl_point_set_state") : set_cuda_error("set_state", e);
+}
+
+extern "C" int paqif_ehl_point_step(paqif_ehl_point* h, int32_t outer, uint32_t flags) {
+  if (!h) return set_arg_error("ehl_point_step");
+  const paqif_ehl_point_cfg& c0 = h->cfg;
+  paqif_ehl_point_cfg c = c0;
+  c.outer = outer;
+  PointDev& d = h->d;
+  const int n = d.n, N = d.N;
+  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
+  cudaStream_t st = h->st;
+  const size_t NN = (size_t)N * N;
+  const size_t smem = h->line_smem;
+  cudaFuncSetAttribute(pt_xline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(pt_xline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(pt_yline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(pt_yline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaMemsetAsync(d.sigma, 0, NN * 8, st);
+  cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
+  cudaMemsetAsync(&d.meta[kMErr], 0, sizeof(int), st);
+  const unsigned fx = (unsigned)((N + 127) / 128);
+  // ---- hybrid x-sweep
+  for (int j = 1; j < n; ++j) {
+    pt_films_kernel<<<dim3(fx, 3), 128, 0, st>>>(d, 0, j - 1, 3);
+    if (exact) pt_xline_kernel<true><<<1, kPtThreads, smem, st>>>(d, c, j);
+    else pt_xline_kernel<false><<<1, kPtThreads, smem, st>>>(d, c, j);
+    fold(h);
+  }
+  pt_weighted_kernel<<<296, 256, 0, st>>>(d, c);
+  pt_copy_kernel<<<296, 256, 0, st>>>(d.u, d.film_out, NN, &d.meta[kMAnyW]);
+  pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 1);
+  fold(h);
+  // ---- column sweep
+  for (int i = 1; i < n; ++i) {
+    const int lo = i - 2 > 0 ? i - 2 : 0;
+    const int L = i + 2 - lo;
+    pt_films_kernel<<<dim3(fx, L), 128, 0, st>>>(d, 1, lo, L);
+    if (exact) pt_yline_kernel<true><<<1, kPtThreads, smem, st>>>(d, c, i);
+    else pt_yline_kernel<false><<<1, kPtThreads, smem, st>>>(d, c, i);
+    fold(h);
+  }
+  // ---- force balance, film, complementarity residual
+  if ((outer + 1) % c.force_every == 0) pt_force_kernel<<<1, 1024, 0, st>>>(d, c);
+  pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 0);
+  fold(h);
+  cudaMemsetAsync(&d.scal[3], 0, sizeof(double), st);
+  pt_residual_kernel<<<N, 256, 0, st>>>(d, c);
+  pt_finish_kernel<<<1, 32, 0, st>>>(d, c);
+  return check_launch("paqif_ehl_point_step");
+}
+
+extern "C" int paqif_ehl_point_get(paqif_ehl_point* h, double* u, double* film, double* scal,
+                                   int32_t* xinfo, int32_t* yinfo, int32_t* err) {
+  if (!h) return set_arg_error("ehl_point_get");
+  const size_t NN = (size_t)h->d.N * h->d.N;
+  cudaStream_t st = h->st;
+  if (u) cudaMemcpyAsync(u, h->d.u, NN * 8, cudaMemcpyDeviceToHost, st);
+  if (film) cudaMemcpyAsync(film, h->d.film_out, NN * 8, cudaMemcpyDeviceToHost, st);
+  if (scal) cudaMemcpyAsync(scal, h->d.scal, 3 * 8, cudaMemcpyDeviceToHost, st);
+  if (xinfo) cudaMemcpyAsync(xinfo, h->d.xinfo, (h->d.n - 1) * 4, cudaMemcpyDeviceToHost, st);
+  if (yinfo) cudaMemcpyAsync(yinfo, h->d.yinfo, (h->d.n - 1) * 4, cudaMemcpyDeviceToHost, st);
+  if (err) cudaMemcpyAsync(err, &h->d.meta[kMErr], 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? PAQIF_OK : set_cuda_error("ehl_point_get", e);
+}
+
+extern "C" int paqif_ehl_point_sync(paqif_ehl_point* h) {
+  if (!h) return set_arg_error("ehl_point_sync");
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? PAQIF_OK : set_cuda_error("ehl_point_sync", e);
+}
+
+extern "C" int paqif_ehl_point_deformation(paqif_ehl_point* h, const double* u, double* out) {
+  if (!h) return set_arg_error("ehl_point_deformation");
+  const size_t NN = (size_t)h->d.N * h->d.N;
+  cudaMemcpyAsync(h->d.film_out, u, NN * 8, cudaMemcpyHostToDevice, h->st);
+  pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
+  fft_deformation(h->plan, h->d.film_out, h->d.dbase, &h->d.meta[kMGate], nullptr, h->st);
+  cudaMemcpyAsync(out, h->d.dbase, NN * 8, cudaMemcpyDeviceToHost, h->st);
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? check_launch("ehl_point_deformation") : set_cuda_error("deformation", e);
+}

@@ -1,9 +1,9 @@
 """Film thickness bookkeeping (public surface of paqif/ehl/film.py:35-155).
 
 Line contact: H = h0 + x^2/2 - (1/pi) sum K*u, the Toeplitz convolution
-running on the GPU (paqif_line_deformation).  Point contact grids carry the
-geometry and kernel tables; their 2-D deformation path is listed as the next
-row in DESIGN.md.
+running on the GPU (paqif_line_deformation).  Point contact: H = h0 +
+(x^2 + y^2)/2 + sum K*u, the 2-D convolution running as an fp64 FFT on the
+GPU (paqif_ehl_point_deformation, csrc/fft_deform.cuh).
 """
 
 from __future__ import annotations
@@ -18,7 +18,7 @@ __all__ = ["FilmModel"]
 
 class FilmModel:
     def __init__(self, contact: str, intervals: int, h: float, lo: float = -2.5,
-                 kernel: DeformationKernel | None = None):
+                 kernel: DeformationKernel | None = None, lo_y: float | None = None):
         if contact not in ("point", "line"):
             raise ContractViolationError("contact must be 'point' or 'line'")
         self.contact = contact
@@ -29,8 +29,11 @@ class FilmModel:
             kernel = (kernel_point(intervals, intervals, h) if contact == "point"
                       else kernel_line(intervals, h))
         self.kernel = kernel
+        # lo_y: the SURVEY 8(c) y-domain adapter, y = (x - x[0]) + lo_y
+        self.y = self.x if lo_y is None else (self.x - self.x[0]) + lo_y
+        self._device = None
         if contact == "point":
-            gx, gy = np.meshgrid(self.x, self.x)
+            gx, gy = np.meshgrid(self.x, self.y)
             self.geometry = 0.5 * (gx ** 2 + gy ** 2)
             self.sign = 1.0
         else:
@@ -40,8 +43,13 @@ class FilmModel:
         self._pending = []
 
     def deformation_full(self, u) -> np.ndarray:
-        if self.contact != "line":
-            raise NotImplementedError("2-D deformation: next row (DESIGN.md section 7)")
+        if self.contact == "point":
+            from .point import PointDevice
+            if self._device is None:
+                self._device = PointDevice(self.kernel.table, self.geometry)
+            self._base = self._device.deformation(u)
+            self._pending = []
+            return self._base
         from .line import line_deformation
         self._base = line_deformation(self.kernel.table, u)
         self._pending = []

@@ -1,0 +1,240 @@
+"""Point-contact Newton steps on the device (configs 4 and 5).
+
+``PointContact`` owns one circular point contact on an (n+1)^2 grid in HBM
+(handle ``paqif_ehl_point``, csrc/ehl_point.cu, C ABI include/paqif_ehl.h)
+and advances it by one outer iteration of solve_ehl per ``step()``:
+the hybrid x-sweep (ehl/solver.py:76-128), the column sweep
+(ehl/sweeps.py:421-518), the force balance every ``force_every`` iterations
+and the complementarity residual.  The 2(n-1) line solves, the exact
+pending-line film corrections and the FFT folds are all device kernels
+enqueued by a native host loop on the handle's stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from .. import _native
+from ..errors import ContractViolationError, FactorizationBreakdownError, PaqifError
+from .kernels import kernel_point
+from .params import EhlParams, hertzian_init
+
+LIMITERS = {"kappa": 0, "none": 1, "van-albada": 2, "minmod": 3, "koren": 4}
+SCHEMES = {"Lhs1": 0, "Lhs2": 1}
+
+
+class PointCfg(ctypes.Structure):
+    """Mirror of paqif_ehl_point_cfg (include/paqif_ehl.h)."""
+    _fields_ = [("n", ctypes.c_int32), ("limiter", ctypes.c_int32),
+                ("variant", ctypes.c_int32), ("compressible", ctypes.c_int32),
+                ("force_every", ctypes.c_int32), ("outer", ctypes.c_int32),
+                ("h", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("omega", ctypes.c_double), ("max_change", ctypes.c_double),
+                ("relax_c", ctypes.c_double), ("max_h0_step", ctypes.c_double),
+                ("load_target", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("z", ctypes.c_double), ("p0", ctypes.c_double),
+                ("p_hertz", ctypes.c_double), ("lam", ctypes.c_double)]
+
+
+def _bind(L):
+    if getattr(L, "_ehl_point_bound", False):
+        return L
+    vp, i32, u32, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_double
+    L.paqif_ehl_point_create.argtypes = [ctypes.POINTER(PointCfg), vp, vp]
+    L.paqif_ehl_point_create.restype = vp
+    L.paqif_ehl_point_destroy.argtypes = [vp]
+    L.paqif_ehl_point_destroy.restype = None
+    L.paqif_ehl_point_set_state.argtypes = [vp, vp, f64]
+    L.paqif_ehl_point_set_state.restype = ctypes.c_int
+    L.paqif_ehl_point_step.argtypes = [vp, i32, u32]
+    L.paqif_ehl_point_step.restype = ctypes.c_int
+    L.paqif_ehl_point_get.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.paqif_ehl_point_get.restype = ctypes.c_int
+    L.paqif_ehl_point_sync.argtypes = [vp]
+    L.paqif_ehl_point_sync.restype = ctypes.c_int
+    L.paqif_ehl_point_deformation.argtypes = [vp, vp, vp]
+    L.paqif_ehl_point_deformation.restype = ctypes.c_int
+    L._ehl_point_bound = True
+    return L
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def point_grid(params: EhlParams, intervals: int):
+    """x, y, h of the point grid (film.py:38-45; y through the lo_y adapter)."""
+    lo, hi = params.domain
+    h = (hi - lo) / intervals
+    x = lo + h * np.arange(intervals + 1)
+    y = x if params.lo_y is None else (x - x[0]) + params.lo_y
+    return x, y, h
+
+
+def point_initial_state(params: EhlParams, intervals: int) -> np.ndarray:
+    """Hertzian hemisphere scaled to the load target, boundary ring zero
+    (solver.py:54-73)."""
+    x, y, _ = point_grid(params, intervals)
+    gx, gy = np.meshgrid(x, y)
+    u = hertzian_init(gx, gy)
+    u[0, :] = u[-1, :] = 0.0
+    u[:, 0] = u[:, -1] = 0.0
+    return u * (params.load_target / (2.0 * np.pi / 3.0))
+
+
+class _Handle:
+    def __init__(self, L, cfg: PointCfg, table: np.ndarray, geometry: np.ndarray):
+        self.L = L
+        t = np.ascontiguousarray(table, dtype=np.float64)
+        g = np.ascontiguousarray(geometry, dtype=np.float64)
+        N = cfg.n + 1
+        if t.shape != (N, N) or g.shape != (N, N):
+            raise ContractViolationError("table and geometry must be (n+1, n+1)")
+        self.ptr = L.paqif_ehl_point_create(ctypes.byref(cfg), _ptr(t), _ptr(g))
+        if not self.ptr:
+            _native.check(-1, "paqif_ehl_point_create")
+
+    def close(self):
+        if self.ptr:
+            self.L.paqif_ehl_point_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PointDevice:
+    """Deformation-only use of the handle (FilmModel('point').deformation_full)."""
+
+    def __init__(self, table: np.ndarray, geometry: np.ndarray):
+        L = _bind(_native.lib())
+        n = table.shape[0] - 1
+        cfg = PointCfg(n=n, force_every=1, h=1.0, p_hertz=1.0, lam=1.0, z=1.0, p0=1.0,
+                       alpha=1.0)
+        self.n = n
+        self.h = _Handle(L, cfg, table, geometry)
+
+    def deformation(self, u) -> np.ndarray:
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        if uu.shape != (self.n + 1, self.n + 1):
+            raise ContractViolationError("u must be (n+1, n+1)")
+        out = np.empty_like(uu)
+        rc = self.h.L.paqif_ehl_point_deformation(self.h.ptr, _ptr(uu), _ptr(out))
+        _native.check(rc, "paqif_ehl_point_deformation")
+        return out
+
+
+class PointContact:
+    """One point contact resident on the GPU, advanced by ``step()``."""
+
+    def __init__(self, params: EhlParams, intervals: int, scheme: str = "Lhs1",
+                 kappa: float = 1 / 3, limiter: str = "kappa", omega: float | None = None,
+                 force_every: int = 5, exact: bool = True, u0=None, h0=None):
+        if params.contact != "point":
+            raise ContractViolationError("PointContact needs a point contact")
+        if scheme not in SCHEMES:
+            raise ContractViolationError(f"unknown scheme {scheme!r}")
+        if limiter not in LIMITERS:
+            raise ContractViolationError(f"unknown limiter {limiter!r}")
+        if not -1.0 <= kappa <= 1.0:
+            raise ContractViolationError("kappa must lie in [-1, 1]")
+        if intervals < 8:
+            raise ContractViolationError("point grid needs at least 8 intervals")
+        self.L = _bind(_native.lib())
+        self.n = int(intervals)
+        x, y, h = point_grid(params, intervals)
+        self.h = h
+        self.x, self.y = x, y
+        gx, gy = np.meshgrid(x, y)
+        self.geometry = 0.5 * (gx ** 2 + gy ** 2)
+        self.table = kernel_point(self.n, self.n, h).table
+        self.cfg = PointCfg(n=self.n, limiter=LIMITERS[limiter], variant=SCHEMES[scheme],
+                            compressible=1 if params.compressible else 0,
+                            force_every=force_every, outer=0, h=h, kappa=kappa,
+                            omega=params.omega if omega is None else omega,
+                            max_change=params.max_change, relax_c=params.relax_c,
+                            max_h0_step=params.max_h0_step, load_target=params.load_target,
+                            alpha=params.alpha, z=params.z, p0=params.p0,
+                            p_hertz=params.p_hertz, lam=params.lam)
+        self.flags = _native.FLAG_EXACT if exact else 0
+        self._h = _Handle(self.L, self.cfg, self.table, self.geometry)
+        if u0 is None:
+            u0 = point_initial_state(params, intervals)
+        self.set_state(u0, params.h0 if h0 is None else h0)
+        self.outer = 0
+
+    def set_state(self, u, h0: float) -> None:
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        if uu.shape != (self.n + 1, self.n + 1):
+            raise ContractViolationError("u must be (n+1, n+1)")
+        rc = self.L.paqif_ehl_point_set_state(self._h.ptr, _ptr(uu), float(h0))
+        _native.check(rc, "paqif_ehl_point_set_state")
+
+    def step(self) -> None:
+        """One outer iteration (asynchronous on the handle's stream)."""
+        rc = self.L.paqif_ehl_point_step(self._h.ptr, self.outer, self.flags)
+        _native.check(rc, "paqif_ehl_point_step")
+        self.outer += 1
+
+    def sync(self) -> None:
+        _native.check(self.L.paqif_ehl_point_sync(self._h.ptr), "paqif_ehl_point_sync")
+
+    def status(self):
+        """(h0, residual, deficit, err) after the last step (synchronises)."""
+        scal = np.zeros(3)
+        err = np.zeros(1, dtype=np.int32)
+        rc = self.L.paqif_ehl_point_get(self._h.ptr, None, None, _ptr(scal), None, None,
+                                        _ptr(err))
+        _native.check(rc, "paqif_ehl_point_get")
+        return float(scal[0]), float(scal[1]), float(scal[2]), int(err[0])
+
+    def snapshot(self):
+        """Host copies: dict(u, film, h0, res, deficit, xinfo, yinfo, err)."""
+        N = self.n + 1
+        u = np.empty((N, N))
+        film = np.empty((N, N))
+        scal = np.zeros(3)
+        xi = np.zeros(self.n - 1, dtype=np.int32)
+        yi = np.zeros(self.n - 1, dtype=np.int32)
+        err = np.zeros(1, dtype=np.int32)
+        rc = self.L.paqif_ehl_point_get(self._h.ptr, _ptr(u), _ptr(film), _ptr(scal), _ptr(xi),
+                                        _ptr(yi), _ptr(err))
+        _native.check(rc, "paqif_ehl_point_get")
+        return dict(u=u, film=film, h0=float(scal[0]), res=float(scal[1]),
+                    deficit=float(scal[2]), newton=(xi & 1).astype(np.int64),
+                    x_rungs=(xi >> 4) & 3, y_rungs=yi, err=int(err[0]))
+
+    @staticmethod
+    def raise_for(err: int) -> None:
+        if err & 5:
+            raise FactorizationBreakdownError(-1, "every rung of a point line solve broke down")
+        if err & 10:
+            raise PaqifError("non-finite change in point-contact sweep")
+
+    def close(self) -> None:
+        self._h.close()
+
+
+def smoke_point_step():
+    """__graft_entry__.smoke() hook: one small point step vs the oracle."""
+    import oracle.ehl_point_oracle as P
+    p = EhlParams.point_from_moes(100.0, 10.0, domain=(-4.5, 1.5), lo_y=-3.0)
+    n = 32
+    pc = PointContact(p, n)
+    pc.step()
+    got = pc.snapshot()
+    c = P.point_case(100.0, 10.0)
+    f = P.PointFilm(n, c)
+    u0 = P.hertz_start(c, f)
+    ur, h0r, fr, rr, info = P.point_step(u0, c.h0, 0, c, f)
+    scale = max(1.0, float(np.max(np.abs(ur))))
+    assert np.array_equal(got["newton"], np.asarray(info["tags"])), "x-sweep Newton tags"
+    assert np.max(np.abs(got["u"] - ur)) <= 1e-9 * scale, "point step parity"
+    assert math.isclose(got["res"], rr, rel_tol=1e-8, abs_tol=1e-12)
+    pc.close()

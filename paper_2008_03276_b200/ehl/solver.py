@@ -1,9 +1,10 @@
 """solve_ehl driver (public surface of paqif/ehl/solver.py:27-240).
 
 The line contact runs every outer iteration as ONE fused CUDA launch
-(LineContactBatch with B = 1); the host only reads back the residual and the
-load deficit for the stop / divergence tests and the ``collect`` callback,
-exactly as the reference loop does (solver.py:210-240).
+(LineContactBatch with B = 1); the point contact as the native sweep driver
+of csrc/ehl_point.cu (PointContact).  The host only reads back the residual
+and the load deficit for the stop / divergence tests and the ``collect``
+callback, exactly as the reference loop does (solver.py:210-240).
 """
 
 from __future__ import annotations
@@ -16,6 +17,7 @@ from ..errors import ContractViolationError, NonConvergenceError, PaqifError
 from .film import FilmModel
 from .line import LineContactBatch, line_initial_state
 from .params import EhlParams
+from .point import PointContact, point_initial_state
 
 __all__ = ["EhlState", "solve_ehl"]
 
@@ -36,10 +38,47 @@ class EhlState:
 def _initial_state(params: EhlParams, intervals: int) -> EhlState:
     lo, hi = params.domain
     h = (hi - lo) / intervals
-    film = FilmModel(params.contact, intervals, h, lo)
-    if params.contact != "line":
-        raise NotImplementedError("point contact: next row (DESIGN.md section 7)")
-    return EhlState(u=line_initial_state(params, intervals), h0=params.h0, film=film)
+    film = FilmModel(params.contact, intervals, h, lo, lo_y=params.lo_y)
+    u = (line_initial_state(params, intervals) if params.contact == "line"
+         else point_initial_state(params, intervals))
+    return EhlState(u=u, h0=params.h0, film=film)
+
+
+class _LineDriver:
+    def __init__(self, params, intervals, state, **kw):
+        self.b = LineContactBatch([params], intervals, u0=state.u[None], h0=[state.h0], **kw)
+
+    def step(self):
+        self.b.step()
+        info = int(self.b.info[0].item())
+        if info & (1 << 8):
+            from ..errors import FactorizationBreakdownError
+            raise FactorizationBreakdownError(-1, "every Ls4 rung broke down")
+        if info & (1 << 3):
+            raise PaqifError("non-finite change in line-contact sweep")
+        deficit = float(self.b.deficit[0].item()) if info & (1 << 2) else None
+        return float(self.b.res[0].item()), deficit
+
+    def state(self):
+        return self.b.u[0].cpu().numpy(), float(self.b.h0[0].item())
+
+
+class _PointDriver:
+    def __init__(self, params, intervals, state, force_every, **kw):
+        self.fe = force_every
+        self.p = PointContact(params, intervals, u0=state.u, h0=state.h0,
+                              force_every=force_every, **kw)
+
+    def step(self):
+        outer = self.p.outer
+        self.p.step()
+        _, res, deficit, err = self.p.status()
+        PointContact.raise_for(err)
+        return res, (deficit if (outer + 1) % self.fe == 0 else None)
+
+    def state(self):
+        snap = self.p.snapshot()
+        return snap["u"], snap["h0"]
 
 
 def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: float = 1 / 3,
@@ -51,35 +90,26 @@ def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: fl
         raise ContractViolationError(f"unknown scheme {scheme!r}")
     if not -1.0 <= kappa <= 1.0:
         raise ContractViolationError("kappa must lie in [-1, 1]")
-    if params.contact != "line":
-        raise NotImplementedError("point contact: next row (DESIGN.md section 7)")
     if state is None:
         state = _initial_state(params, intervals)
-    batch = LineContactBatch([params], intervals, scheme=scheme, kappa=kappa, limiter=limiter,
-                             omega=omega, force_every=force_every, exact=exact,
-                             u0=state.u[None], h0=[state.h0])
+    kw = dict(scheme=scheme, kappa=kappa, limiter=limiter, omega=omega,
+              force_every=force_every, exact=exact)
+    drv = (_LineDriver(params, intervals, state, **kw) if params.contact == "line"
+           else _PointDriver(params, intervals, state, **kw))
     grow = 0
     best = np.inf
     try:
         for outer in range(max_outer):
-            batch.step()
-            res = float(batch.res[0].item())
-            info = int(batch.info[0].item())
-            if info & (1 << 8):
-                from ..errors import FactorizationBreakdownError
-                raise FactorizationBreakdownError(-1, "every Ls4 rung broke down")
-            if info & (1 << 3):
-                raise PaqifError("non-finite change in line-contact sweep")
-            if info & (1 << 2):
-                deficit = float(batch.deficit[0].item())
+            res, fb = drv.step()
+            if fb is not None:
+                deficit = fb
                 state.force_history.append(abs(deficit))
             else:
                 deficit = state.force_history[-1] if state.force_history else np.inf
             state.residual_history.append(res)
             state.outer_iterations = outer + 1
             if collect is not None:
-                state.u = batch.u[0].cpu().numpy()
-                state.h0 = float(batch.h0[0].item())
+                state.u, state.h0 = drv.state()
                 collect(state, res, deficit)
             if res <= tol and abs(deficit) <= tol_fb:
                 return state
@@ -94,5 +124,4 @@ def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: fl
         raise NonConvergenceError("contact iteration exhausted its budget",
                                   residual=state.residual_history[-1], iterations=max_outer)
     finally:
-        state.u = batch.u[0].cpu().numpy()
-        state.h0 = float(batch.h0[0].item())
+        state.u, state.h0 = drv.state()
