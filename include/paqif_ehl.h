@@ -56,6 +56,13 @@ int paqif_ehl_line_step(const paqif_ehl_line_cfg *cfg, int64_t B, const double *
                         double *film, double *res, double *deficit, int32_t *info,
                         uint32_t flags, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Complementarity residual max|min(u, -R(u))|/h and film of B line states
+ * (EhlState.complementarity_residual / film_field, ehl/solver.py:40-51);
+ * [dev] pointers as in paqif_ehl_line_step, film may be NULL. */
+int paqif_ehl_line_residual(const paqif_ehl_line_cfg *cfg, int64_t B, const double *table,
+                            const double *p_hertz, const double *lam, const double *u,
+                            const double *h0, double *film, double *res, void *stream);
+
 /* Line deformation  d_b[i] = -(1/pi) sum_j table[|i-j|] u_b[j]  for B pressure
  * vectors of n+1 nodes (FilmModel.deformation_full, ehl/film.py:67-71). */
 int paqif_line_deformation(int64_t B, int64_t n, const double *table /*[dev] n+1*/,
@@ -102,9 +109,30 @@ int paqif_ehl_point_set_state(paqif_ehl_point *h, const double *u, double h0);
 /* Enqueues one outer iteration (asynchronous on the handle's stream). */
 int paqif_ehl_point_step(paqif_ehl_point *h, int32_t outer, uint32_t flags);
 
+/* Enqueues one sweep of the public sweep functions on the resident state:
+ *   kind 0  _hybrid_x_sweep         (ehl/solver.py:76-128)
+ *   kind 1  newton_line_sweep       (ehl/sweeps.py:344-379; immediate updates)
+ *   kind 2  weighted_change_sweep   (ehl/sweeps.py:382-418; deferred, spread)
+ *   kind 3  column_sweep            (ehl/sweeps.py:421-518)
+ * sel: line system of the x-sweeps, -1 by min(eps)/h > 0.6 (hybrid_select),
+ * 0 Newton (Ls0/Ls1), 1 weighted (Ls4/Ls5); nu_variant 0 Ls1/Ls4, 1 Ls0/Ls5
+ * (kernel_nu); omega the under-relaxation.  The sweep's worst |resid|
+ * (the functions' return value) is reported by _get. */
+int paqif_ehl_point_sweep(paqif_ehl_point *h, int32_t kind, int32_t sel, int32_t nu_variant,
+                          double omega, uint32_t flags);
+
+/* force_balance_update (ehl/sweeps.py:521-535), enqueued. */
+int paqif_ehl_point_force_balance(paqif_ehl_point *h);
+
+/* EhlState.complementarity_residual and film_full (ehl/solver.py:40-51),
+ * enqueued; read with _get. */
+int paqif_ehl_point_residual(paqif_ehl_point *h);
+
 /* Synchronises and copies results to HOST buffers (any may be NULL):
- *   u, film (n+1)^2;  scal[3] = {h0, complementarity residual, deficit};
- *   xinfo (n-1): bit 0 Newton line, bits 4..5 ladder rung (3 = failed);
+ *   u, film (n+1)^2;  scal[4] = {h0, complementarity residual, deficit of the
+ *   last force balance, worst |resid| of the last sweep / step};
+ *   xinfo (n-1): bit 0 Newton system (Ls0/Ls1), bit 1 deferred update,
+ *                bits 4..5 ladder rung (3 = failed);
  *   yinfo (n-1): rung (0 tridiagonal, 1 diagonal, 3 failed);
  *   err: bit 0/2 an x/y line broke down on every rung, 1/3 non-finite change */
 int paqif_ehl_point_get(paqif_ehl_point *h, double *u, double *film, double *scal,

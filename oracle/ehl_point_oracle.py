@@ -12,6 +12,8 @@ Reference functions restated (paths under /root/reference/pkg/src/paqif):
   assemble_line_system (point terms)   ehl/sweeps.py:157-267
   robust_line_solve / _solve_line      ehl/sweeps.py:270-295
   _hybrid_x_sweep                      ehl/solver.py:76-128
+  newton_line_sweep                    ehl/sweeps.py:344-379
+  weighted_change_sweep                ehl/sweeps.py:382-418
   column_sweep                         ehl/sweeps.py:421-518
   force_balance_update (h^2 weight)    ehl/sweeps.py:521-535
   reynolds_residual_field (2-D),
@@ -297,12 +299,69 @@ def hybrid_x_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="k
     return u, tags, rungs
 
 
-def column_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kappa"):
+def newton_line_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kappa",
+                      scheme="Ls1", omega=None, hybrid=None):
+    """sweeps.newton_line_sweep (sweeps.py:344-379): immediate updates, the
+    line system fixed or picked per line by hybrid_select.  Returns
+    (u, worst |resid|)."""
     n = u.shape[0] - 1
     h = film.h
-    omega = c.omega
+    omega = c.omega if omega is None else omega
+    worst = 0.0
+    for j in range(1, n):
+        args, eps_line = line_quantities(u, film, c, j, h0, kappa, limiter)
+        sch = scheme
+        if hybrid is not None:
+            pair = ("Ls1", "Ls4") if hybrid == "Lhs1" else ("Ls0", "Ls5")
+            sch = pair[0] if float(np.min(eps_line)) / h > SWITCH else pair[1]
+        sig, _ = robust_solve(args, film, h, kappa, limiter, sch)
+        sig = np.clip(sig, -c.max_change, c.max_change)
+        new = np.maximum(0.0, u[j, 1:n] + omega * sig)
+        delta = np.zeros(n + 1)
+        delta[1:n] = new - u[j, 1:n]
+        u[j, 1:n] = new
+        film.note("row", j, delta, u)
+        worst = max(worst, float(np.max(np.abs(args[-1]))))
+    return u, worst
+
+
+def weighted_change_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kappa",
+                          scheme="Ls4", omega=None):
+    """sweeps.weighted_change_sweep (sweeps.py:382-418): every line against
+    the sweep-start state, changes spread to the 4 neighbours at the end.
+    Returns (u, worst |resid|)."""
+    n = u.shape[0] - 1
+    h = film.h
+    omega = c.omega if omega is None else omega
+    sigma = np.zeros_like(u)
+    worst = 0.0
+    for j in range(1, n):
+        args, _ = line_quantities(u, film, c, j, h0, kappa, limiter)
+        sig, _ = robust_solve(args, film, h, kappa, limiter, scheme)
+        sigma[j, 1:n] = np.clip(sig, -c.max_change, c.max_change)
+        worst = max(worst, float(np.max(np.abs(args[-1]))))
+    spread = np.zeros_like(sigma)
+    spread[:, 1:] += sigma[:, :-1]
+    spread[:, :-1] += sigma[:, 1:]
+    spread[1:, :] += sigma[:-1, :]
+    spread[:-1, :] += sigma[1:, :]
+    u = np.maximum(0.0, u + omega * (sigma - 0.25 * spread))
+    u[0, :] = u[-1, :] = 0.0
+    u[:, 0] = u[:, -1] = 0.0
+    film.deformation_full(u)
+    return u, worst
+
+
+def column_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kappa",
+                 omega=None, stats=None):
+    """sweeps.column_sweep (sweeps.py:421-518).  Returns (u, rungs); the
+    worst |resid| goes to stats['worst'] when a dict is passed."""
+    n = u.shape[0] - 1
+    h = film.h
+    omega = c.omega if omega is None else omega
     s = film.sens
     rungs = []
+    worst = 0.0
     for i in range(1, n):
         lo = max(0, i - 2)
         films = film.cols(list(range(lo, i + 2)), h0)
@@ -362,6 +421,9 @@ def column_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kap
         delta[1:n] = new - u[1:n, i]
         u[1:n, i] = new
         film.note("col", i, delta, u)
+        worst = max(worst, float(np.max(np.abs(resid))))
+    if stats is not None:
+        stats["worst"] = worst
     return u, rungs
 
 
@@ -382,6 +444,14 @@ def residual_field(u, fv, c: PointCase, film: PointFilm, kappa, limiter):
         r[j, i] = (exp_ * (u[j, i + 1] - u[j, i]) + exm * (u[j, i - 1] - u[j, i])) / h \
             + (eyp * (u[j + 1, i] - u[j, i]) + eym * (u[j - 1, i] - u[j, i])) / h - h * fd
     return r
+
+
+def complementarity_residual(u, h0, c: PointCase, film: PointFilm, kappa=1 / 3,
+                             limiter="kappa"):
+    """EhlState.complementarity_residual (solver.py:43-51), point contact."""
+    fv = film.film_full(u, h0)
+    r = residual_field(u, fv, c, film, kappa, limiter)
+    return float(np.max(np.abs(np.minimum(u, -r)))) / (film.h * film.h)
 
 
 def point_step(u, h0, outer, c: PointCase, film: PointFilm, kappa=1 / 3, limiter="kappa",

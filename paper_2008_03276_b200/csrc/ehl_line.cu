@@ -173,6 +173,76 @@ __device__ void assemble_row(int i, const double* rho, const double* eps, const 
   }
 }
 
+// complementarity residual max|min(u, -R(u))| of a pressure (solver.py:43-51,
+// sweeps.py:106-123) with its film; returns the CTA-wide (NaN-propagating) max
+__device__ double line_comp_residual(const paqif_ehl_line_cfg& c, double h0, const double* sun,
+                                     const double* sdef, double ph, double lam, double* sfilm,
+                                     double* seps, double* sq, double* red) {
+  const int n = c.n, N = n + 1;
+  const double h = c.h;
+  const double sign = -1.0 / 3.141592653589793;
+  double qmax = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const double x = c.lo + h * (double)i;
+    const double fv = (h0 + 0.5 * (x * x)) + sign * sdef[i];
+    double rho, eps;
+    rheology(sun[i], fv, c, ph, lam, rho, eps);
+    sfilm[i] = fv;
+    seps[i] = eps;
+    sq[i] = rho * fv;
+    qmax = fmax(qmax, fabs(rho * fv));
+  }
+  const double gfloor2 = 1e-12 * fmax(block_max(qmax, red), kRatioGuard);
+  double comp = 0.0;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double r = 0.0;
+    if (i >= 1 && i <= n - 1) {
+      const double dqi = sq[i + 1] - sq[i], dqm = sq[i] - sq[i - 1];
+      const double php = limiter_wplus(gratio(dqi, dqm, gfloor2), c.limiter, c.kappa);
+      double phm = 0.0;
+      if (i >= 2) {
+        const double dqmm = sq[i - 1] - sq[i - 2];
+        phm = limiter_wplus(gratio(dqm, dqmm, gfloor2), c.limiter, c.kappa);
+      }
+      const double fd = (sq[i] + 0.5 * php * dqi) - (sq[i - 1] + 0.5 * phm * dqm);
+      const double e_p = 0.5 * (seps[i] + seps[i + 1]);
+      const double e_m = 0.5 * (seps[i] + seps[i - 1]);
+      r = (e_p * (sun[i + 1] - sun[i]) + e_m * (sun[i - 1] - sun[i])) / h - fd;
+    }
+    const double m = fabs(np_minimum(sun[i], -r));
+    comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+  }
+  return block_nanmax(comp, red);
+}
+
+// residual-only pass (EhlState.complementarity_residual for line states)
+__global__ void __launch_bounds__(kEhlThreads)
+ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
+                         const double* __restrict__ p_hertz, const double* __restrict__ lamv,
+                         const double* u_in, const double* h0_in, double* film_out,
+                         double* res_out) {
+  extern __shared__ __align__(16) double esm[];
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  const int n = c.n, N = n + 1;
+  const EhlSmemLayout L(n);
+  double* ext = esm + L.ext;
+  double* su = esm + L.su;
+  double* sdef = esm + L.def;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_in[b * N + k];
+  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
+    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  __syncthreads();
+  toeplitz_conv(su, ext, n, 1.0, sdef);
+  __syncthreads();
+  const double cmax = line_comp_residual(c, h0_in[b], su, sdef, p_hertz[b], lamv[b],
+                                         esm + L.film, esm + L.eps, esm + L.q, esm + L.red);
+  if (film_out)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) film_out[b * N + i] = esm[L.film + i];
+  if (threadIdx.x == 0) res_out[b] = cmax / c.h;
+}
+
 template <bool EXACT>
 __global__ void __launch_bounds__(kEhlThreads)
 ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
@@ -355,39 +425,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     fb = 1;
     deficit_v = deficit;
   }
-  qmax = 0.0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const double x = c.lo + h * (double)i;
-    const double fv = (h0 + 0.5 * (x * x)) + sign * sdef[i];
-    double rho, eps;
-    rheology(sun[i], fv, c, ph, lam, rho, eps);
-    sfilm[i] = fv;
-    seps[i] = eps;
-    sq[i] = rho * fv;
-    qmax = fmax(qmax, fabs(rho * fv));
-  }
-  const double gfloor2 = 1e-12 * fmax(block_max(qmax, red), kRatioGuard);
-  double comp = 0.0;
-  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double r = 0.0;
-    if (i >= 1 && i <= n - 1) {
-      const double dqi = sq[i + 1] - sq[i], dqm = sq[i] - sq[i - 1];
-      const double php = limiter_wplus(gratio(dqi, dqm, gfloor2), c.limiter, c.kappa);
-      double phm = 0.0;
-      if (i >= 2) {
-        const double dqmm = sq[i - 1] - sq[i - 2];
-        phm = limiter_wplus(gratio(dqm, dqmm, gfloor2), c.limiter, c.kappa);
-      }
-      const double fd = (sq[i] + 0.5 * php * dqi) - (sq[i - 1] + 0.5 * phm * dqm);
-      const double e_p = 0.5 * (seps[i] + seps[i + 1]);
-      const double e_m = 0.5 * (seps[i] + seps[i - 1]);
-      r = (e_p * (sun[i + 1] - sun[i]) + e_m * (sun[i - 1] - sun[i])) / h - fd;
-    }
-    const double m = fabs(np_minimum(sun[i], -r));
-    comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
-  }
-  const double cmax = block_nanmax(comp, red);
+  const double cmax = line_comp_residual(c, h0, sun, sdef, ph, lam, sfilm, seps, sq, red);
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     u_io[b * N + i] = sun[i];
     film_out[b * N + i] = sfilm[i];
@@ -470,4 +508,21 @@ extern "C" int paqif_line_deformation(int64_t B, int64_t n, const double* table,
   cudaFuncSetAttribute(line_deformation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   line_deformation_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>((int)n, table, u, out);
   return check_launch("paqif_line_deformation");
+}
+
+extern "C" int paqif_ehl_line_residual(const paqif_ehl_line_cfg* cfg, int64_t B,
+                                       const double* table, const double* p_hertz,
+                                       const double* lam, const double* u, const double* h0,
+                                       double* film, double* res, void* stream)
+{
+  if (!cfg || B < 0 || cfg->n < 4 || !res) return set_arg_error("ehl_line_residual: bad args");
+  if (B == 0) return PAQIF_OK;
+  const EhlSmemLayout L(cfg->n);
+  const size_t smem = (size_t)L.total * 8;
+  if (smem > 227 * 1024) return set_arg_error("ehl_line_residual: grid too fine for one CTA");
+  cudaFuncSetAttribute(ehl_line_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  ehl_line_residual_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>(
+      *cfg, B, table, p_hertz, lam, u, h0, film, res);
+  return check_launch("paqif_ehl_line_residual");
 }

@@ -30,6 +30,14 @@ constexpr int kPtThreads = 256;
 constexpr int kMaxPending = 9;
 enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMSize = 24 };
 
+// per-sweep controls (the public sweep variants of sweeps.py / solver.py)
+struct SweepCtl {
+  int sel;         // assembly: -1 by min(eps)/h (hybrid), 0 Newton (Ls0/Ls1), 1 weighted (Ls4/Ls5)
+  int defer;       // update: -1 deferred iff weighted (_hybrid_x_sweep), 0 immediate, 1 deferred
+  int nu_variant;  // 0 Ls1/Ls4 kernel strength, 1 Ls0/Ls5 (kernel_nu)
+  double omega;
+};
+
 struct PointDev {
   int n, N, n_sys;
   double* u;
@@ -40,7 +48,7 @@ struct PointDev {
   double* sigma;    // N x N
   double* pend;     // kMaxPending x N
   int* meta;        // kMSize ints
-  double* scal;     // [0] h0, [1] res, [2] deficit, [3] comp max bits
+  double* scal;     // [0] h0, [1] res, [2] deficit, [3] comp max bits, [4] worst |resid| bits
   double* scratch;  // line solve scratch
   int32_t* xinfo;   // n-1: newton tag | rung << 4
   int32_t* yinfo;   // n-1: rung
@@ -169,6 +177,14 @@ __device__ __forceinline__ void point_row(double rw, double rc, double re, doubl
   }
 }
 
+// worst |resid| of the sweep (python max over lines ignores NaN lines)
+__device__ __forceinline__ void note_worst(PointDev& d, double v, double* red) {
+  const double m = block_max(v, red);
+  if (threadIdx.x == 0 && m > 0.0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&d.scal[4]),
+              (unsigned long long)__double_as_longlong(m));
+}
+
 struct PtShared {
   double red[32];
   int flag;
@@ -192,7 +208,7 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
 // (sweeps.py:318-341) and assemble_line_system's point terms (sweeps.py:157-267)
 template <bool EXACT>
 __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
-                                                              int j) {
+                                                              SweepCtl ctl, int j) {
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
   EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(xsm + sizeof(PtShared) / 8);
@@ -215,12 +231,13 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
   }
   const double ratio = block_min(emin, S.red) / h;
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
-  const bool newton = ratio > kSwitch;
-  const bool weighted = !newton;
+  const bool weighted = ctl.sel < 0 ? !(ratio > kSwitch) : ctl.sel == 1;
+  const bool deferred = ctl.defer < 0 ? weighted : ctl.defer == 1;
+  const bool newton = !deferred;  // immediate update (and pending note)
   // kernel sensitivities (film.sensitivity, point: table[|d|][|off|])
   const double* t = d.table;
   const double s00 = t[0], s10 = t[N], s20 = t[2 * N], s01 = t[1], s11 = t[N + 1];
-  const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
+  const double nu = ctl.nu_variant == 0 ? (2.0 - c.kappa) / 2.0
                                    : (2.0 - c.kappa) / 2.0 + (1.0 - c.kappa) / 4.0;
   double ks0, ks1;
   if (weighted) {
@@ -234,6 +251,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
   double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
   int rung = 0;
   int st = 1;
+  double worst = 0.0;
   for (; rung < 3; ++rung) {
     for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
       double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
@@ -264,16 +282,18 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
              (ey_p * (u[(size_t)(j + 1) * N + i] - uc) + ey_m * (u[(size_t)(j - 1) * N + i] - uc)) / h -
              h * fd;
         point_row(rw, rc, re, ex_p, ex_m, ey_p, ey_m, php, phm, h, weighted, rung, ks0, ks1, e);
+        worst = fmax(worst, fabs(rr));
       }
       put_row(band, rhs, n_sys, n_int, r, e, rr);
     }
+    if (rung == 0) note_worst(d, worst, S.red);
     st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
     if (!st) break;
   }
   if (st) {
     if (threadIdx.x == 0) {
       atomicOr(&d.meta[kMErr], 1);
-      d.xinfo[j - 1] = (newton ? 1 : 0) | (3 << 4);
+      d.xinfo[j - 1] = (weighted ? 0 : 1) | (deferred ? 2 : 0) | (3 << 4);
     }
     return;
   }
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
       sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
       if (newton) {
         const double old = u[(size_t)j * N + i];
-        const double nv = np_maximum(0.0, old + c.omega * sg);
+        const double nv = np_maximum(0.0, old + ctl.omega * sg);
         const double dl = nv - old;
         nz |= (dl != 0.0) || (dl != dl);
         delta[i] = dl;
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
   fin = __syncthreads_and(fin);
   if (threadIdx.x == 0) {
     if (!fin) atomicOr(&d.meta[kMErr], 2);
-    d.xinfo[j - 1] = (newton ? 1 : 0) | (rung << 4);
+    d.xinfo[j - 1] = (weighted ? 0 : 1) | (deferred ? 2 : 0) | (rung << 4);
     if (newton && nz) {  // note_line_update("row", j, delta, u)
       const int p = d.meta[kMCount];
       d.meta[kMAxis + p] = 0;
@@ -311,12 +331,12 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
       d.meta[kMCount] = p + 1;
       if (p + 1 > 8) d.meta[kMGate] = 1;
     }
-    if (weighted) d.meta[kMAnyW] = 1;
+    if (deferred) d.meta[kMAnyW] = 1;
   }
 }
 
 // deferred weighted changes of the x-sweep (solver.py:115-127)
-__global__ void pt_weighted_kernel(PointDev d, paqif_ehl_point_cfg c) {
+__global__ void pt_weighted_kernel(PointDev d, double omega) {
   if (d.meta[kMAnyW] == 0) return;
   const int N = d.N, n = d.n;
   const size_t total = (size_t)N * N;
@@ -329,7 +349,7 @@ __global__ void pt_weighted_kernel(PointDev d, paqif_ehl_point_cfg c) {
     if (i < n) sp += s[g + 1];
     if (j >= 1) sp += s[g - N];
     if (j < n) sp += s[g + N];
-    double v = np_maximum(0.0, d.u[g] + c.omega * (s[g] - 0.25 * sp));
+    double v = np_maximum(0.0, d.u[g] + omega * (s[g] - 0.25 * sp));
     if (i == 0 || i == n || j == 0 || j == n) v = 0.0;
     d.film_out[g] = v;  // staged: u must not change while neighbours are read
   }
@@ -349,7 +369,7 @@ __global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
 // column i of column_sweep (sweeps.py:437-517)
 template <bool EXACT>
 __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
-                                                              int i) {
+                                                              SweepCtl ctl, int i) {
   extern __shared__ __align__(16) double ysm[];
   PtShared& S = *reinterpret_cast<PtShared*>(ysm);
   EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(ysm + sizeof(PtShared) / 8);
@@ -377,6 +397,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
   double* band = d.scratch;
   double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
   int st = 1, rung = 0;
+  double worst = 0.0;
   for (; rung < 2; ++rung) {  // 0: tridiagonal system, 1: diagonal fallback
     for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
       double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
@@ -406,6 +427,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
         rr = (ex_p * (u[(size_t)jj * N + i + 1] - uc) + ex_m * (u[(size_t)jj * N + i - 1] - uc)) / h +
              (ey_p * (u[(size_t)(jj + 1) * N + i] - uc) + ey_m * (u[(size_t)(jj - 1) * N + i] - uc)) / h -
              h * (flux_p - flux_m);
+        worst = fmax(worst, fabs(rr));
         if (rung == 0) {
           const double a_p = 1.0 - 0.5 * php, b_p = 0.5 * php;
           const double a_m = 1.0 - 0.5 * phm, b_m = 0.5 * phm;
@@ -430,6 +452,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
       }
       put_row(band, rhs, n_sys, n_int, r, e, rr);
     }
+    if (rung == 0) note_worst(d, worst, S.red);
     st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
     if (!st) break;
   }
@@ -449,7 +472,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
       fin &= isfinite(sg);
       sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
       const double old = u[(size_t)m * N + i];
-      const double nv = np_maximum(0.0, old + c.omega * sg);
+      const double nv = np_maximum(0.0, old + ctl.omega * sg);
       const double dl = nv - old;
       nz |= (dl != 0.0) || (dl != dl);
       delta[m] = dl;
@@ -673,52 +696,110 @@ extern "C" int paqif_ehl_point_set_state(paqif_ehl_point* h, const double* u, do
   return e == cudaSuccess ? check_launch("ehl_point_set_state") : set_cuda_error("set_state", e);
 }
 
-extern "C" int paqif_ehl_point_step(paqif_ehl_point* h, int32_t outer, uint32_t flags) {
-  if (!h) return set_arg_error("ehl_point_step");
-  const paqif_ehl_point_cfg& c0 = h->cfg;
-  paqif_ehl_point_cfg c = c0;
-  c.outer = outer;
+namespace {
+
+void prepare_attrs(paqif_ehl_point* h) {
+  static bool done = false;  // per process; attributes are per function
+  if (done) return;
+  const int smem = (int)h->line_smem;
+  cudaFuncSetAttribute(pt_xline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_xline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_yline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_yline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done = true;
+}
+
+// x-direction sweep: lines j = 1..n-1 in order, each followed by the gated
+// fold; deferred changes applied (and folded) at the end.
+void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   PointDev& d = h->d;
   const int n = d.n, N = d.N;
-  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
   cudaStream_t st = h->st;
   const size_t NN = (size_t)N * N;
-  const size_t smem = h->line_smem;
-  cudaFuncSetAttribute(pt_xline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(pt_xline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(pt_yline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(pt_yline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned fx = (unsigned)((N + 127) / 128);
   cudaMemsetAsync(d.sigma, 0, NN * 8, st);
   cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
-  cudaMemsetAsync(&d.meta[kMErr], 0, sizeof(int), st);
-  const unsigned fx = (unsigned)((N + 127) / 128);
-  // ---- hybrid x-sweep
   for (int j = 1; j < n; ++j) {
     pt_films_kernel<<<dim3(fx, 3), 128, 0, st>>>(d, 0, j - 1, 3);
-    if (exact) pt_xline_kernel<true><<<1, kPtThreads, smem, st>>>(d, c, j);
-    else pt_xline_kernel<false><<<1, kPtThreads, smem, st>>>(d, c, j);
+    if (exact) pt_xline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+    else pt_xline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
     fold(h);
   }
-  pt_weighted_kernel<<<296, 256, 0, st>>>(d, c);
-  pt_copy_kernel<<<296, 256, 0, st>>>(d.u, d.film_out, NN, &d.meta[kMAnyW]);
-  pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 1);
-  fold(h);
-  // ---- column sweep
+  if (ctl.defer != 0) {
+    pt_weighted_kernel<<<296, 256, 0, st>>>(d, ctl.omega);
+    pt_copy_kernel<<<296, 256, 0, st>>>(d.u, d.film_out, NN, &d.meta[kMAnyW]);
+    pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 1);
+    fold(h);
+  }
+}
+
+void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
+  PointDev& d = h->d;
+  const int n = d.n, N = d.N;
+  cudaStream_t st = h->st;
+  const unsigned fx = (unsigned)((N + 127) / 128);
   for (int i = 1; i < n; ++i) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
     pt_films_kernel<<<dim3(fx, L), 128, 0, st>>>(d, 1, lo, L);
-    if (exact) pt_yline_kernel<true><<<1, kPtThreads, smem, st>>>(d, c, i);
-    else pt_yline_kernel<false><<<1, kPtThreads, smem, st>>>(d, c, i);
+    if (exact) pt_yline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+    else pt_yline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
     fold(h);
   }
-  // ---- force balance, film, complementarity residual
-  if ((outer + 1) % c.force_every == 0) pt_force_kernel<<<1, 1024, 0, st>>>(d, c);
+}
+
+void enqueue_residual(paqif_ehl_point* h) {
+  PointDev& d = h->d;
+  cudaStream_t st = h->st;
   pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 0);
-  fold(h);
+  fold(h);  // film_full: fresh deformation, pending list cleared
   cudaMemsetAsync(&d.scal[3], 0, sizeof(double), st);
-  pt_residual_kernel<<<N, 256, 0, st>>>(d, c);
-  pt_finish_kernel<<<1, 32, 0, st>>>(d, c);
+  pt_residual_kernel<<<d.N, 256, 0, st>>>(d, h->cfg);
+  pt_finish_kernel<<<1, 32, 0, st>>>(d, h->cfg);
+}
+
+}  // namespace
+
+extern "C" int paqif_ehl_point_sweep(paqif_ehl_point* h, int32_t kind, int32_t sel,
+                                     int32_t nu_variant, double omega, uint32_t flags) {
+  if (!h) return set_arg_error("ehl_point_sweep");
+  if (kind < 0 || kind > 3 || sel < -1 || sel > 1 || nu_variant < 0 || nu_variant > 1)
+    return set_arg_error("ehl_point_sweep: kind/sel/nu_variant");
+  prepare_attrs(h);
+  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
+  cudaMemsetAsync(&h->d.meta[kMErr], 0, sizeof(int), h->st);
+  cudaMemsetAsync(&h->d.scal[4], 0, sizeof(double), h->st);
+  SweepCtl ctl{sel, kind == 0 ? -1 : (kind == 2 ? 1 : 0), nu_variant, omega};
+  if (kind == 3) enqueue_y_sweep(h, ctl, exact);
+  else enqueue_x_sweep(h, ctl, exact);
+  return check_launch("paqif_ehl_point_sweep");
+}
+
+extern "C" int paqif_ehl_point_force_balance(paqif_ehl_point* h) {
+  if (!h) return set_arg_error("ehl_point_force_balance");
+  pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, h->cfg);
+  return check_launch("paqif_ehl_point_force_balance");
+}
+
+extern "C" int paqif_ehl_point_residual(paqif_ehl_point* h) {
+  if (!h) return set_arg_error("ehl_point_residual");
+  enqueue_residual(h);
+  return check_launch("paqif_ehl_point_residual");
+}
+
+extern "C" int paqif_ehl_point_step(paqif_ehl_point* h, int32_t outer, uint32_t flags) {
+  if (!h) return set_arg_error("ehl_point_step");
+  prepare_attrs(h);
+  const paqif_ehl_point_cfg& c = h->cfg;
+  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
+  cudaMemsetAsync(&h->d.meta[kMErr], 0, sizeof(int), h->st);
+  cudaMemsetAsync(&h->d.scal[4], 0, sizeof(double), h->st);
+  // solve_ehl (solver.py:205-216): hybrid x-sweep, column sweep, force
+  // balance every force_every-th iteration, complementarity residual
+  enqueue_x_sweep(h, SweepCtl{-1, -1, c.variant, c.omega}, exact);
+  enqueue_y_sweep(h, SweepCtl{0, 0, c.variant, c.omega}, exact);
+  if ((outer + 1) % c.force_every == 0) pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, c);
+  enqueue_residual(h);
   return check_launch("paqif_ehl_point_step");
 }
 
@@ -729,7 +810,10 @@ extern "C" int paqif_ehl_point_get(paqif_ehl_point* h, double* u, double* film, 
   cudaStream_t st = h->st;
   if (u) cudaMemcpyAsync(u, h->d.u, NN * 8, cudaMemcpyDeviceToHost, st);
   if (film) cudaMemcpyAsync(film, h->d.film_out, NN * 8, cudaMemcpyDeviceToHost, st);
-  if (scal) cudaMemcpyAsync(scal, h->d.scal, 3 * 8, cudaMemcpyDeviceToHost, st);
+  if (scal) {
+    cudaMemcpyAsync(scal, h->d.scal, 3 * 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(scal + 3, h->d.scal + 4, 8, cudaMemcpyDeviceToHost, st);
+  }
   if (xinfo) cudaMemcpyAsync(xinfo, h->d.xinfo, (h->d.n - 1) * 4, cudaMemcpyDeviceToHost, st);
   if (yinfo) cudaMemcpyAsync(yinfo, h->d.yinfo, (h->d.n - 1) * 4, cudaMemcpyDeviceToHost, st);
   if (err) cudaMemcpyAsync(err, &h->d.meta[kMErr], 4, cudaMemcpyDeviceToHost, st);

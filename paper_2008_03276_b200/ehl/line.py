@@ -43,6 +43,9 @@ def _bind(L):
     L.paqif_ehl_line_step.argtypes = [ctypes.POINTER(LineCfg), i64, vp, vp, vp, vp, vp, vp, vp,
                                       vp, vp, u32, vp, sz, vp]
     L.paqif_ehl_line_step.restype = ctypes.c_int
+    L.paqif_ehl_line_residual.argtypes = [ctypes.POINTER(LineCfg), i64, vp, vp, vp, vp, vp, vp,
+                                          vp, vp]
+    L.paqif_ehl_line_residual.restype = ctypes.c_int
     L.paqif_line_deformation.argtypes = [i64, i64, vp, vp, vp, vp]
     L.paqif_line_deformation.restype = ctypes.c_int
     L._ehl_bound = True
@@ -132,6 +135,18 @@ class LineContactBatch:
                                         _native.stream_ptr(stream))
         _native.check(rc, "paqif_ehl_line_step")
         self.outer += 1
+
+    def residual(self, stream=None) -> np.ndarray:
+        """Complementarity residual of every case's current state (host array)."""
+        torch = _native.torch_cuda()
+        out = torch.empty(self.B, dtype=torch.float64, device="cuda")
+        rc = self.L.paqif_ehl_line_residual(ctypes.byref(self.cfg), self.B, self.table.data_ptr(),
+                                            self.p_hertz.data_ptr(), self.lam.data_ptr(),
+                                            self.u.data_ptr(), self.h0.data_ptr(),
+                                            self.film.data_ptr(), out.data_ptr(),
+                                            _native.stream_ptr(stream))
+        _native.check(rc, "paqif_ehl_line_residual")
+        return out.cpu().numpy()
 
     def snapshot(self):
         """Host copies: (u, h0, film, res, deficit, info)."""

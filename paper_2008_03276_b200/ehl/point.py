@@ -55,6 +55,12 @@ def _bind(L):
     L.paqif_ehl_point_get.restype = ctypes.c_int
     L.paqif_ehl_point_sync.argtypes = [vp]
     L.paqif_ehl_point_sync.restype = ctypes.c_int
+    L.paqif_ehl_point_sweep.argtypes = [vp, i32, i32, i32, f64, u32]
+    L.paqif_ehl_point_sweep.restype = ctypes.c_int
+    L.paqif_ehl_point_force_balance.argtypes = [vp]
+    L.paqif_ehl_point_force_balance.restype = ctypes.c_int
+    L.paqif_ehl_point_residual.argtypes = [vp]
+    L.paqif_ehl_point_residual.restype = ctypes.c_int
     L.paqif_ehl_point_deformation.argtypes = [vp, vp, vp]
     L.paqif_ehl_point_deformation.restype = ctypes.c_int
     L._ehl_point_bound = True
@@ -182,12 +188,30 @@ class PointContact:
         _native.check(rc, "paqif_ehl_point_step")
         self.outer += 1
 
+    def sweep(self, kind: int, sel: int = -1, nu_variant: int | None = None,
+              omega: float | None = None) -> None:
+        """One public sweep on the resident state (kinds: 0 hybrid x, 1 Newton
+        x, 2 weighted x, 3 column; see include/paqif_ehl.h)."""
+        nu = self.cfg.variant if nu_variant is None else nu_variant
+        om = self.cfg.omega if omega is None else omega
+        rc = self.L.paqif_ehl_point_sweep(self._h.ptr, kind, sel, nu, float(om), self.flags)
+        _native.check(rc, "paqif_ehl_point_sweep")
+
+    def force_balance(self) -> None:
+        _native.check(self.L.paqif_ehl_point_force_balance(self._h.ptr),
+                      "paqif_ehl_point_force_balance")
+
+    def residual(self) -> float:
+        """complementarity_residual of the resident state (synchronises)."""
+        _native.check(self.L.paqif_ehl_point_residual(self._h.ptr), "paqif_ehl_point_residual")
+        return self.status()[1]
+
     def sync(self) -> None:
         _native.check(self.L.paqif_ehl_point_sync(self._h.ptr), "paqif_ehl_point_sync")
 
     def status(self):
         """(h0, residual, deficit, err) after the last step (synchronises)."""
-        scal = np.zeros(3)
+        scal = np.zeros(4)
         err = np.zeros(1, dtype=np.int32)
         rc = self.L.paqif_ehl_point_get(self._h.ptr, None, None, _ptr(scal), None, None,
                                         _ptr(err))
@@ -195,11 +219,12 @@ class PointContact:
         return float(scal[0]), float(scal[1]), float(scal[2]), int(err[0])
 
     def snapshot(self):
-        """Host copies: dict(u, film, h0, res, deficit, xinfo, yinfo, err)."""
+        """Host copies: dict(u, film, h0, res, deficit, worst, newton, deferred,
+        x_rungs, y_rungs, err)."""
         N = self.n + 1
         u = np.empty((N, N))
         film = np.empty((N, N))
-        scal = np.zeros(3)
+        scal = np.zeros(4)
         xi = np.zeros(self.n - 1, dtype=np.int32)
         yi = np.zeros(self.n - 1, dtype=np.int32)
         err = np.zeros(1, dtype=np.int32)
@@ -207,7 +232,8 @@ class PointContact:
                                         _ptr(yi), _ptr(err))
         _native.check(rc, "paqif_ehl_point_get")
         return dict(u=u, film=film, h0=float(scal[0]), res=float(scal[1]),
-                    deficit=float(scal[2]), newton=(xi & 1).astype(np.int64),
+                    deficit=float(scal[2]), worst=float(scal[3]),
+                    newton=(xi & 1).astype(np.int64), deferred=((xi >> 1) & 1).astype(np.int64),
                     x_rungs=(xi >> 4) & 3, y_rungs=yi, err=int(err[0]))
 
     @staticmethod

@@ -34,6 +34,15 @@ class EhlState:
     def film_field(self) -> np.ndarray:
         return self.film.film_full(self.u, self.h0)
 
+    def complementarity_residual(self, params, kappa, limiter) -> float:
+        """max |min(u, -r)| / h^d of the current state (solver.py:43-51)."""
+        if self.film.contact == "point":
+            from .sweeps import _device_contact
+            return _device_contact(self, params, kappa, limiter).residual()
+        b = LineContactBatch([params], self.film.n, kappa=kappa, limiter=limiter,
+                             u0=np.asarray(self.u)[None], h0=[self.h0])
+        return b.residual()[0]
+
 
 def _initial_state(params: EhlParams, intervals: int) -> EhlState:
     lo, hi = params.domain

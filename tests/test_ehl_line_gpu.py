@@ -126,3 +126,18 @@ def test_solve_ehl_line_api():
     for k in range(3):
         ur, h0r, _, rr, _ = E.line_step(ur, h0r, k, c, film)
         assert math.isclose(seen[k], rr, rel_tol=1e-8)
+
+
+@pytest.mark.parametrize("key", KEYS[:3])
+def test_line_complementarity_residual(key):
+    """EhlState.complementarity_residual for a line state equals the residual
+    the reference reports after its step (residual-only kernel)."""
+    from paper_2008_03276_b200.ehl import solver
+    d = gcase(key)
+    p = params_for(d)
+    n = int(d["meta"][2])
+    st = solver._initial_state(p, n)
+    st.u = d["u_out"].copy()
+    st.h0 = float(d["h0_out"])
+    assert math.isclose(st.complementarity_residual(p, 1.0 / 3.0, "kappa"), float(d["res_out"]),
+                        rel_tol=TOL)

@@ -121,3 +121,37 @@ def test_no_host_fallback(monkeypatch):
     pc = PointContact(params_for(100.0), 32)
     pc.step()
     assert math.isfinite(pc.status()[1])
+
+
+S = load_golden("ehl_point_sweeps.npz")
+SWEEPS = sorted({k.split("__")[0] for k in S.files})
+
+
+@pytest.mark.parametrize("name", SWEEPS)
+def test_public_sweeps_vs_reference(name):
+    """newton_line_sweep / weighted_change_sweep / column_sweep /
+    complementarity_residual on an EhlState (reference signatures)."""
+    from paper_2008_03276_b200.ehl import sweeps
+    from paper_2008_03276_b200.ehl.solver import _initial_state
+    d = {k.split("__", 1)[1]: S[k] for k in S.files if k.startswith(name + "__")}
+    src = gcase(str(d["src"]))
+    m, l, n, _ = src["meta"]
+    p = params_for(float(m), float(l))
+    st = _initial_state(p, int(n))
+    st.u = src["u_in"].copy()
+    st.h0 = float(src["h0_in"])
+    call, lim, kappa = str(d["call"]), str(d["limiter"]), 1.0 / 3.0
+    if call == "newton":
+        hyb = str(d["hybrid"]) or None
+        val = sweeps.newton_line_sweep(st, p, kappa, lim, scheme=str(d["scheme"]) or "Ls1",
+                                       hybrid=hyb)
+    elif call == "weighted":
+        val = sweeps.weighted_change_sweep(st, p, kappa, lim, scheme=str(d["scheme"]))
+    elif call == "column":
+        val = sweeps.column_sweep(st, p, kappa, lim)
+    else:
+        val = st.complementarity_residual(p, kappa, lim)
+    ref = d["u_out"]
+    assert close_field(st.u, ref)
+    assert np.array_equal(st.u == 0.0, ref == 0.0)
+    assert math.isclose(val, float(d["value"]), rel_tol=TOL)

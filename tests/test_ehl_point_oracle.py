@@ -36,3 +36,45 @@ def test_point_step_matches_reference(key):
     assert np.array_equal(u == 0.0, d["u_out"] == 0.0)
     assert h0 == pytest.approx(float(d["h0_out"]), rel=1e-13)
     assert res == pytest.approx(float(d["res_out"]), rel=1e-9)
+
+
+S = load_golden("ehl_point_sweeps.npz")
+SWEEPS = sorted({k.split("__")[0] for k in S.files})
+
+
+def sweep_case(name):
+    d = {k.split("__", 1)[1]: S[k] for k in S.files if k.startswith(name + "__")}
+    src = gcase(str(d["src"]))
+    return d, src
+
+
+def run_oracle_sweep(d, src):
+    m, l, n, k = src["meta"]
+    c = P.PointCase(p_hertz=float(src["p_hertz"]), lam=float(src["lam"]))
+    film = P.PointFilm(int(n), c)
+    u = src["u_in"].copy()
+    h0 = float(src["h0_in"])
+    film.deformation_full(u)
+    call, lim = str(d["call"]), str(d["limiter"])
+    kappa = 1.0 / 3.0
+    if call == "newton":
+        hyb = str(d["hybrid"]) or None
+        return P.newton_line_sweep(u, h0, film, c, kappa, lim, scheme=str(d["scheme"]) or "Ls1",
+                                   hybrid=hyb)
+    if call == "weighted":
+        return P.weighted_change_sweep(u, h0, film, c, kappa, lim, scheme=str(d["scheme"]))
+    if call == "column":
+        st = {}
+        u, _ = P.column_sweep(u, h0, film, c, kappa, lim, stats=st)
+        return u, st["worst"]
+    return u, P.complementarity_residual(u, h0, c, film, kappa, lim)
+
+
+@pytest.mark.parametrize("name", SWEEPS)
+def test_sweep_functions_match_reference(name):
+    d, src = sweep_case(name)
+    u, val = run_oracle_sweep(d, src)
+    ref = d["u_out"]
+    assert np.max(np.abs(u - ref)) <= 1e-11 * max(1.0, float(np.max(np.abs(ref))))
+    assert np.array_equal(u == 0.0, ref == 0.0)
+    assert val == pytest.approx(float(d["value"]), rel=1e-10)

@@ -1,0 +1,9 @@
+"""One point-contact outer iteration (for ncu launch lists)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2008_03276_b200.ehl import EhlParams, PointContact
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+m = 100.0 if n <= 512 else 1000.0
+pc = PointContact(EhlParams.point_from_moes(m, 10.0, domain=(-4.5, 1.5), lo_y=-3.0), n)
+pc.step()
+print("res", pc.status()[1])
