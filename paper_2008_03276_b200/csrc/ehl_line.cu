@@ -17,14 +17,13 @@
 //
 // The Toeplitz convolution is register-tiled (4 outputs per thread, one
 // shared-memory kernel value and one broadcast pressure per 4 DFMA); the
-// banded solve runs on one warp through the same AQIF engine as the LCP
-// path (aqif_warp.cuh) with the line system staged in the case's
-// workspace.  Elementwise formulas follow numpy's operation order; the
+// banded solve runs on one warp through the beta=2 latency engine
+// (aqif2.cuh) with the line system, right side and pivot records in shared
+// memory (in the case's workspace when n is too large for that).  Elementwise formulas follow numpy's operation order; the
 // convolution and the load sum use a different summation order than
 // numpy's BLAS dot / pairwise sum (documented tolerance).
 #include <cfloat>
-#include "aqif_warp.cuh"
-#include "zsolve.cuh"
+#include "aqif2.cuh"
 #include "ehl_common.cuh"
 #include "capi_util.cuh"
 
@@ -33,35 +32,16 @@ namespace paqif {
 constexpr int kEhlThreads = 256;
 constexpr int kEhlBeta = 2;
 
-struct EhlLinePol {
-  static constexpr bool kFuseW = true;
-  static constexpr bool kResidual = false;
-  static constexpr bool kRecordW = false;
-  using PL = PivotLayout<kEhlBeta>;
-  const double* band;
-  const double* rhs;
-  double* zs;
-  int n;
-  __device__ __forceinline__ const double* raw_ptr(int i, int d) const {
-    return band + (size_t)(d + kEhlBeta) * n + i;
-  }
-  __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
-  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
-  __device__ __forceinline__ bool pinned(int) const { return false; }
-  __device__ __forceinline__ const double* frhs_ptr(int i) const { return rhs + i; }
-  __device__ __forceinline__ double frhs(int i) const { return rhs[i]; }
-  __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
-    double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
-    const double2* src = reinterpret_cast<const double2*>(pb);
-    for (int idx = gl; idx < PL::kSize / 2; idx += G) dst[idx] = src[idx];
-  }
-  __device__ __forceinline__ void on_w(int, int, double, double) {}
-  __device__ __forceinline__ void on_resid(int, int, double) {}
-};
-
 struct EhlSmemLayout {
   // offsets in doubles
-  int ext, su, sun, film, rho, eps, q, php, phm, res, sig, def, red, eng, ring, total;
+  // band/rhs/rec: the line system (5 x n_sys), its right side and the AQIF
+  // pivot records, when they fit (sys_in_smem); else in the workspace
+  int ext, su, sun, film, rho, eps, q, php, phm, res, sig, def, red, band, rhs, rec, total;
+  bool sys_in_smem;
+  __host__ __device__ static int nsys(int n) {
+    const int n_int = n - 1;
+    return (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+  }
   __host__ __device__ explicit EhlSmemLayout(int n) {
     const int N = n + 1, NA = (N + 3 + 1) & ~1;  // padded for the 4-wide conv tail
     int o = 0;
@@ -78,8 +58,11 @@ struct EhlSmemLayout {
     sig = o; o += NA;
     def = o; o += NA;
     red = o; o += 32;
-    eng = o; o += (int)(sizeof(EngineSmem<kEhlBeta>) / 8) + 2;
-    ring = o; o += ZChunk<kEhlBeta>::kRing;
+    const int ns = nsys(n);
+    const int sys = 5 * ns + ns + (ns / 2 + 1) * kRec2;
+    sys_in_smem = (size_t)(o + sys) * 8 <= 227 * 1024;
+    band = o; rhs = o + 5 * ns; rec = rhs + ns;
+    if (sys_in_smem) o += sys;
     total = o;
   }
 };
@@ -269,14 +252,12 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   double* ssig = esm + L.sig;
   double* sdef = esm + L.def;
   double* red = esm + L.red;
-  EngineSmem<kEhlBeta>& eng = *reinterpret_cast<EngineSmem<kEhlBeta>*>(esm + L.eng);
-  double* ring = esm + L.ring;
-  // workspace of this case
-  char* my = ws + (size_t)b * ws_per_case;
-  double* band = reinterpret_cast<double*>(my);
+  // line system: shared memory, or this case's workspace for large n
+  double* wsd = reinterpret_cast<double*>(ws + (size_t)b * ws_per_case);
+  double* band = L.sys_in_smem ? esm + L.band : wsd;
   double* rhs = band + (size_t)(2 * kEhlBeta + 1) * n_sys;
-  double* xsol = rhs + n_sys;
-  double* zs = xsol + n_sys;
+  double* rec = rhs + n_sys;
+  double* xsol = band;  // x overwrites the band after the factor
   const double ph = p_hertz[b], lam = lamv[b];
   const double h = c.h;
   const double sign = -1.0 / 3.141592653589793;
@@ -358,24 +339,9 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     }
     if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
     __syncthreads();
-    // solve on warp 0 (group 0 of the engine; the other groups idle)
-    int fst = 0, zst = 0;
-    if (threadIdx.x < 32) {
-      constexpr int G = Group<kEhlBeta>::G;
-      const int lane = threadIdx.x;
-      const bool alive = lane < G;
-      EhlLinePol pol{band, rhs, zs, n_sys};
-      fst = aqif_factor_group<kEhlBeta, EXACT>(pol, n_sys, 1e-14, eng, lane % G, alive);
-      fst = __shfl_sync(0xffffffffu, fst, 0);
-      if (fst == 0) {
-        zst = zsolve_group<kEhlBeta, EXACT, true>(zs, n_sys, xsol, ring, lane % G, alive);
-        zst = __shfl_sync(0xffffffffu, zst, 0);
-      }
-      if (lane == 0) red[31] = (fst || zst) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    st = red[31] != 0.0;
-    __syncthreads();
+    // solve on warp 0 (aqif2: factor + fused W, Z outside-in)
+    int* flag = reinterpret_cast<int*>(red + 30);
+    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, xsol, flag) & 1;
     if (!st) break;
   }
   if (st) {
@@ -449,8 +415,9 @@ extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
   const int64_t n_int = n - 1;
   const int64_t n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
   const int64_t s = n_sys / 2;
-  const size_t per = ((size_t)(2 * kEhlBeta + 1) * n_sys + 2 * n_sys +
-                      (size_t)(s + 1) * PivotLayout<kEhlBeta>::kSize + 32) * 8;
+  // the line system lives in shared memory when it fits (EhlSmemLayout)
+  if (n <= (1 << 20) && EhlSmemLayout((int)n).sys_in_smem) return (size_t)B * 256;
+  const size_t per = ((size_t)(2 * kEhlBeta + 1) * n_sys + n_sys + (size_t)(s + 1) * kRec2 + 32) * 8;
   return (size_t)B * ((per + 255) & ~(size_t)255);
 }
 

@@ -14,9 +14,10 @@
 // line solve on warp 0 with the reference's fallback ladder, clip, immediate
 // update or deferred weighted change, pending note) -> gated fold.
 #include <cfloat>
+#include <cstdlib>
 #include <vector>
 #include "ehl_common.cuh"
-#include "ehl_solve.cuh"
+#include "aqif2.cuh"
 #include "fft_deform.cuh"
 #include "capi_util.cuh"
 
@@ -27,6 +28,11 @@ extern "C" {
 namespace paqif {
 
 constexpr int kPtThreads = 256;
+constexpr int kLineBeta = 2;
+// line system (5 x n_sys band, right side, AQIF pivot records), doubles
+__host__ __device__ inline size_t pt_sys_doubles(int n_sys) {
+  return (size_t)(2 * kLineBeta + 1) * n_sys + n_sys + (size_t)(n_sys / 2 + 1) * kRec2;
+}
 constexpr int kMaxPending = 9;
 enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMSize = 24 };
 
@@ -49,7 +55,9 @@ struct PointDev {
   double* pend;     // kMaxPending x N
   int* meta;        // kMSize ints
   double* scal;     // [0] h0, [1] res, [2] deficit, [3] comp max bits, [4] worst |resid| bits
-  double* scratch;  // line solve scratch
+  double* scratch;  // line system when it does not fit in shared memory
+  int sys_in_smem;
+  unsigned long long* prof;  // dev phase timing (PAQIF_PT_PROF=1), else null
   int32_t* xinfo;   // n-1: newton tag | rung << 4
   int32_t* yinfo;   // n-1: rung
   double* film_out; // N x N
@@ -72,37 +80,57 @@ __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_eh
   return coeff * (gap * gap * gap);
 }
 
-// films of `L` consecutive rows (mode 0) or columns (mode 1) starting at `first`
-__global__ void pt_films_kernel(PointDev d, int mode, int first, int L) {
+// films of `L` consecutive rows (mode 0) or columns (mode 1) starting at
+// `first` (FilmModel.film_rows / film_cols, film.py:98-146).  With pending
+// line updates every output is a length-N dot product per update: one warp
+// per output, lanes striding the sum (coalesced table/delta reads), four
+// independent accumulators, shuffle reduction.  Without pending updates a
+// thread per output.  Launch: kPtFilmWarps warps per block, enough blocks
+// for L*N warps.
+constexpr int kPtFilmWarps = 8;
+__global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d, int mode,
+                                                                     int first, int L) {
   const int N = d.N;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y;
-  if (idx >= N || l >= L) return;
-  const int line = first + l;
-  const double h0 = d.scal[0];
   const int count = d.meta[kMCount];
-  const size_t g = mode == 0 ? (size_t)line * N + idx : (size_t)idx * N + line;
-  double v = (h0 + d.geom[g]) + d.dbase[g];
-  if (count > 0) {
-    double corr = 0.0;
-    for (int p = 0; p < count; ++p) {
-      const int axis = d.meta[kMAxis + p], ell = d.meta[kMIdx + p];
-      const double* delta = d.pend + (size_t)p * N;
-      double s = 0.0;
-      if (axis == mode) {
-        // same axis: 1-D Toeplitz convolution with the kernel row |line-ell|
-        const double* tr = d.table + (size_t)abs(line - ell) * N;
-        for (int k = 0; k < N; ++k) s = fma(tr[abs(idx - k)], delta[k], s);
-      } else {
-        // cross axis: gather-matvec (film.py:114-117, 131-134; symmetric table)
-        const double* tr = d.table + (size_t)abs(idx - ell) * N;
-        for (int k = 0; k < N; ++k) s = fma(tr[abs(line - k)], delta[k], s);
-      }
-      corr += s;
-    }
-    v = v + corr;
+  const double h0 = d.scal[0];
+  auto base = [&](int line, int idx) {
+    const size_t g = mode == 0 ? (size_t)line * N + idx : (size_t)idx * N + line;
+    return (h0 + d.geom[g]) + d.dbase[g];
+  };
+  if (count == 0) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < L * N) d.films[o] = base(first + o / N, o % N);
+    return;
   }
-  d.films[(size_t)l * N + idx] = v;
+  const int lane = threadIdx.x & 31;
+  const int o = blockIdx.x * kPtFilmWarps + (threadIdx.x >> 5);
+  if (o >= L * N) return;
+  const int l = o / N, idx = o % N;
+  const int line = first + l;
+  double corr = 0.0;
+  for (int p = 0; p < count; ++p) {
+    const int axis = d.meta[kMAxis + p], ell = d.meta[kMIdx + p];
+    const double* __restrict__ delta = d.pend + (size_t)p * N;
+    // same axis: Toeplitz row |line-ell| at |idx-k|; cross axis: kernel row
+    // |idx-ell| at |line-k| (film.py:114-117, 131-134; symmetric table)
+    const bool same = axis == mode;
+    const double* __restrict__ tr = d.table + (size_t)abs(same ? line - ell : idx - ell) * N;
+    const int c = same ? idx : line;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int k = lane;
+    for (; k + 96 < N; k += 128) {
+      a0 = fma(tr[abs(c - k)], delta[k], a0);
+      a1 = fma(tr[abs(c - k - 32)], delta[k + 32], a1);
+      a2 = fma(tr[abs(c - k - 64)], delta[k + 64], a2);
+      a3 = fma(tr[abs(c - k - 96)], delta[k + 96], a3);
+    }
+    for (; k < N; k += 32) a0 = fma(tr[abs(c - k)], delta[k], a0);
+    double sp = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, off);
+    corr += sp;
+  }
+  if (lane == 0) d.films[o] = base(line, idx) + corr;
 }
 
 __device__ __forceinline__ double block_min(double v, double* red) {
@@ -211,12 +239,12 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
                                                               SweepCtl ctl, int j) {
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
-  EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(xsm + sizeof(PtShared) / 8);
-  double* ring = xsm + sizeof(PtShared) / 8 + sizeof(EngineSmem<kLineBeta>) / 8;
+  double* sysb = d.sys_in_smem ? xsm + sizeof(PtShared) / 8 : d.scratch;
   const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
   const double h = c.h;
   const double* u = d.u;
   const double* F = d.films;  // rows j-1, j, j+1
+  long long tp0 = clock64(), tp1 = 0, tp2 = 0, tp3 = 0;
   auto film = [&](int r, int i) { return F[(size_t)(r - (j - 1)) * N + i]; };
   auto eps_at = [&](int r, int i, double& rho) {
     return rheo_eps(u[(size_t)r * N + i], film(r, i), c, rho);
@@ -231,6 +259,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
   }
   const double ratio = block_min(emin, S.red) / h;
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
+  tp1 = clock64();
   const bool weighted = ctl.sel < 0 ? !(ratio > kSwitch) : ctl.sel == 1;
   const bool deferred = ctl.defer < 0 ? weighted : ctl.defer == 1;
   const bool newton = !deferred;  // immediate update (and pending note)
@@ -247,8 +276,9 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
     ks0 = s00;
     ks1 = s10;
   }
-  double* band = d.scratch;
+  double* band = sysb;
   double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
+  double* rec = rhs + n_sys;
   int rung = 0;
   int st = 1;
   double worst = 0.0;
@@ -287,8 +317,18 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
       put_row(band, rhs, n_sys, n_int, r, e, rr);
     }
     if (rung == 0) note_worst(d, worst, S.red);
-    st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
+    if (rung == 0) tp2 = clock64();
+    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, band, &S.flag);
+    if (rung == 0) tp3 = clock64();
+    if (d.prof && threadIdx.x == 0 && (st & 2)) atomicAdd(&d.prof[5], 1ull);
+    st &= 1;
     if (!st) break;
+  }
+  if (d.prof && threadIdx.x == 0) {
+    atomicAdd(&d.prof[0], (unsigned long long)(tp1 - tp0));
+    atomicAdd(&d.prof[1], (unsigned long long)(tp2 - tp1));
+    atomicAdd(&d.prof[2], (unsigned long long)(tp3 - tp2));
+    atomicAdd(&d.prof[4], 1ull);
   }
   if (st) {
     if (threadIdx.x == 0) {
@@ -297,7 +337,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
     }
     return;
   }
-  const double* x = line_solution(d.scratch, n_sys);
+  const double* x = band;  // aqif2_solve wrote x over the band
   int nz = 0, fin = 1;
   double* delta = d.pend + (size_t)d.meta[kMCount] * N;  // next pending slot (used if newton)
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -332,6 +372,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_
       if (p + 1 > 8) d.meta[kMGate] = 1;
     }
     if (deferred) d.meta[kMAnyW] = 1;
+    if (d.prof) atomicAdd(&d.prof[3], (unsigned long long)(clock64() - tp3));
   }
 }
 
@@ -372,8 +413,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
                                                               SweepCtl ctl, int i) {
   extern __shared__ __align__(16) double ysm[];
   PtShared& S = *reinterpret_cast<PtShared*>(ysm);
-  EngineSmem<kLineBeta>& eng = *reinterpret_cast<EngineSmem<kLineBeta>*>(ysm + sizeof(PtShared) / 8);
-  double* ring = ysm + sizeof(PtShared) / 8 + sizeof(EngineSmem<kLineBeta>) / 8;
+  double* sysb = d.sys_in_smem ? ysm + sizeof(PtShared) / 8 : d.scratch;
   const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
   const double h = c.h;
   const int lo = i - 2 > 0 ? i - 2 : 0;
@@ -394,8 +434,9 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
   const double* t = d.table;
   const double s00 = t[0], s10 = t[N], s01 = t[1], s11 = t[N + 1];
-  double* band = d.scratch;
+  double* band = sysb;
   double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
+  double* rec = rhs + n_sys;
   int st = 1, rung = 0;
   double worst = 0.0;
   for (; rung < 2; ++rung) {  // 0: tridiagonal system, 1: diagonal fallback
@@ -453,7 +494,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
       put_row(band, rhs, n_sys, n_int, r, e, rr);
     }
     if (rung == 0) note_worst(d, worst, S.red);
-    st = solve_line_system<EXACT>(d.scratch, n_sys, eng, ring, &S.flag);
+    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, band, &S.flag) & 1;
     if (!st) break;
   }
   if (st) {
@@ -463,7 +504,7 @@ __global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_
     }
     return;
   }
-  const double* x = line_solution(d.scratch, n_sys);
+  const double* x = band;  // aqif2_solve wrote x over the band
   int nz = 0, fin = 1;
   double* delta = d.pend + (size_t)d.meta[kMCount] * N;
   for (int m = threadIdx.x; m < N; m += blockDim.x) {
@@ -636,10 +677,15 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.pend = dalloc<double>(h, (size_t)kMaxPending * N);
   d.meta = dalloc<int>(h, kMSize);
   d.scal = dalloc<double>(h, 8);
-  d.scratch = dalloc<double>(h, line_scratch_doubles(n_sys));
+  const size_t sys_bytes = pt_sys_doubles(n_sys) * sizeof(double);
+  d.sys_in_smem = sizeof(PtShared) + sys_bytes <= 227 * 1024;
+  d.scratch = dalloc<double>(h, d.sys_in_smem ? 32 : pt_sys_doubles(n_sys));
   d.xinfo = dalloc<int32_t>(h, N);
   d.yinfo = dalloc<int32_t>(h, N);
   d.film_out = dalloc<double>(h, NN);
+  d.prof = nullptr;
+  if (const char* e = getenv("PAQIF_PT_PROF"))
+    if (e[0] == '1') d.prof = dalloc<unsigned long long>(h, 8);
   FftPlan& p = h->plan;
   p.n = n;
   p.P = fft_size_for(n);
@@ -656,7 +702,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != 17) {
+  if (h->allocs.size() != (d.prof ? 18u : 17u)) {
     paqif_ehl_point_destroy(h);
     set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
     return nullptr;
@@ -665,8 +711,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   cudaMemcpyAsync(d.geom, geometry, NN * 8, cudaMemcpyHostToDevice, h->st);
   fft_prepare(p.P);
   fft_plan_kernel(p, d.table, h->st);
-  h->line_smem = sizeof(PtShared) + sizeof(EngineSmem<kLineBeta>) +
-                 ZChunk<kLineBeta>::kRing * sizeof(double);
+  h->line_smem = sizeof(PtShared) + (d.sys_in_smem ? sys_bytes : 0);
   if (cudaStreamSynchronize(h->st) != cudaSuccess || check_launch("ehl_point_create")) {
     paqif_ehl_point_destroy(h);
     return nullptr;
@@ -677,6 +722,13 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
 extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
   if (!h) return;
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->d.prof) {
+    unsigned long long pr[8] = {0};
+    cudaMemcpy(pr, h->d.prof, sizeof(pr), cudaMemcpyDeviceToHost);
+    const double nl = pr[4] ? (double)pr[4] : 1.0;
+    fprintf(stderr, "[pt_prof] x-lines %llu (checked repeats %llu): cycles/line pass1 %.0f assemble %.0f solve %.0f update %.0f\n",
+            pr[4], pr[5], pr[0] / nl, pr[1] / nl, pr[2] / nl, pr[3] / nl);
+  }
   for (void* a : h->allocs)
     if (a) cudaFree(a);
   if (h->st) cudaStreamDestroy(h->st);
@@ -698,10 +750,15 @@ extern "C" int paqif_ehl_point_set_state(paqif_ehl_point* h, const double* u, do
 
 namespace {
 
+unsigned film_blocks(int N, int L) {
+  return (unsigned)((L * N + kPtFilmWarps - 1) / kPtFilmWarps);
+}
+
 void prepare_attrs(paqif_ehl_point* h) {
   static bool done = false;  // per process; attributes are per function
   if (done) return;
-  const int smem = (int)h->line_smem;
+  (void)h;
+  const int smem = 227 * 1024;  // the largest any handle asks for
   cudaFuncSetAttribute(pt_xline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pt_xline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pt_yline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -716,11 +773,10 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   const int n = d.n, N = d.N;
   cudaStream_t st = h->st;
   const size_t NN = (size_t)N * N;
-  const unsigned fx = (unsigned)((N + 127) / 128);
   cudaMemsetAsync(d.sigma, 0, NN * 8, st);
   cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
   for (int j = 1; j < n; ++j) {
-    pt_films_kernel<<<dim3(fx, 3), 128, 0, st>>>(d, 0, j - 1, 3);
+    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(d, 0, j - 1, 3);
     if (exact) pt_xline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
     else pt_xline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
     fold(h);
@@ -737,11 +793,10 @@ void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   PointDev& d = h->d;
   const int n = d.n, N = d.N;
   cudaStream_t st = h->st;
-  const unsigned fx = (unsigned)((N + 127) / 128);
   for (int i = 1; i < n; ++i) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
-    pt_films_kernel<<<dim3(fx, L), 128, 0, st>>>(d, 1, lo, L);
+    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(d, 1, lo, L);
     if (exact) pt_yline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
     else pt_yline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
     fold(h);
