@@ -168,7 +168,7 @@ def config3_cases(rank, count=1024, seed=SEED):
     return out
 
 
-def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5):
+def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1)):
     """EHL Newton-step throughput: config 1 (one line contact, N=513) and
     config 3 (1024 line contacts per GPU, N=1025), device-timed per outer
     iteration, plus the oracle CPU rate on this host."""
@@ -230,6 +230,58 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5):
         out["config3"]["cpu_baseline"] = {"value": 1.0 / dt3, "unit": "case-iters/s",
                                           "cores": 1, "kind": "port",
                                           "sample": f"{k} oracle steps of case 0, one core"}
+    out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
+    return out
+
+
+def point_secondary(with_cpu, steps4=3, steps5=1):
+    """EHL point contact, one outer iteration of solve_ehl per step through
+    the native sweep driver (csrc/ehl_point.cu): config 4 (513^2, M=100) and
+    config 5 (2049^2, M=1000), device-timed on the handle's stream."""
+    import torch
+    from paper_2008_03276_b200.ehl import EhlParams, PointContact
+    out = {}
+
+    def run(n, m, steps, warm):
+        p = EhlParams.point_from_moes(m, 10.0, domain=(-4.5, 1.5), lo_y=-3.0)
+        pc = PointContact(p, n)
+        for _ in range(warm):
+            pc.step()
+        pc.sync()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        stream = torch.cuda.ExternalStream(pc.stream_handle())
+        e0.record(stream)
+        for _ in range(steps):
+            pc.step()
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        snap = pc.snapshot()
+        pc.close()
+        return ms, snap
+
+    if steps4 > 0:
+        ms4, s4 = run(512, 100.0, steps4, 3)
+        out["config4"] = {"metric": "EHL point Newton iters/s (513x513, M=100, L=10)",
+                          "value": 1e3 / ms4, "unit": "iters/s", "ms_per_iter": ms4,
+                          "lines_per_iter": 2 * 511, "newton_x_lines_last": int(s4["newton"].sum()),
+                          "residual_last": s4["res"]}
+        if with_cpu:
+            import oracle.ehl_point_oracle as P
+            c = P.point_case(100.0, 10.0)
+            f = P.PointFilm(512, c)
+            t0 = time.perf_counter()
+            P.point_step(P.hertz_start(c, f), c.h0, 0, c, f)
+            dt = time.perf_counter() - t0
+            out["config4"]["cpu_baseline"] = {"value": 1.0 / dt, "unit": "iters/s", "cores": 1,
+                                              "kind": "port",
+                                              "sample": "1 oracle point iteration (numpy/scipy)"}
+    if steps5 > 0:
+        ms5, s5 = run(2048, 1000.0, steps5, 1)
+        out["config5"] = {"metric": "EHL point Newton iters/s (2049x2049, M=1000, L=10)",
+                          "value": 1e3 / ms5, "unit": "iters/s", "ms_per_iter": ms5,
+                          "lines_per_iter": 2 * 2047, "residual_last": s5["res"]}
     return out
 
 
@@ -276,7 +328,8 @@ def main():
     ap.add_argument("--fast", action="store_true", help="FMA arithmetic (default: exact)")
     ap.add_argument("--batch", type=int, default=B_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-ehl", action="store_true", help="skip the config-1/3 EHL lines")
+    ap.add_argument("--no-ehl", action="store_true", help="skip the config-1/3/4/5 EHL lines")
+    ap.add_argument("--no-point", action="store_true", help="skip the config-4/5 point lines")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -409,7 +462,8 @@ def main():
     }
     if not args.no_ehl:
         line["secondary"] = ehl_secondary(rank, world, with_cpu=(rank == 0 and world == 1
-                                                                  and not args.no_cpu_baseline))
+                                                                  and not args.no_cpu_baseline),
+                                          point_steps=(0, 0) if args.no_point else (3, 1))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
         sample = 1024

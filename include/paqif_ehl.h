@@ -139,6 +139,9 @@ int paqif_ehl_point_get(paqif_ehl_point *h, double *u, double *film, double *sca
                         int32_t *xinfo, int32_t *yinfo, int32_t *err);
 int paqif_ehl_point_sync(paqif_ehl_point *h);
 
+/* The handle's CUDA stream (cudaStream_t), for event timing and ordering. */
+void *paqif_ehl_point_stream(paqif_ehl_point *h);
+
 /* Deformation of HOST pressure u into HOST out (FilmModel.deformation_full). */
 int paqif_ehl_point_deformation(paqif_ehl_point *h, const double *u, double *out);
 

@@ -227,7 +227,7 @@ ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restri
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kEhlThreads)
+__global__ void __launch_bounds__(kEhlThreads, 1)
 ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                 const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
                 double* h0_io, double* film_out, double* res_out, double* deficit_out,

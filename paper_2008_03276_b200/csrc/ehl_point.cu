@@ -235,7 +235,7 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
 // x-line j of _hybrid_x_sweep (solver.py:91-114) with _line_quantities
 // (sweeps.py:318-341) and assemble_line_system's point terms (sweeps.py:157-267)
 template <bool EXACT>
-__global__ void __launch_bounds__(kPtThreads) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
+__global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int j) {
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
@@ -409,7 +409,7 @@ __global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
 
 // column i of column_sweep (sweeps.py:437-517)
 template <bool EXACT>
-__global__ void __launch_bounds__(kPtThreads) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
+__global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int i) {
   extern __shared__ __align__(16) double ysm[];
   PtShared& S = *reinterpret_cast<PtShared*>(ysm);
@@ -728,6 +728,11 @@ extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
     const double nl = pr[4] ? (double)pr[4] : 1.0;
     fprintf(stderr, "[pt_prof] x-lines %llu (checked repeats %llu): cycles/line pass1 %.0f assemble %.0f solve %.0f update %.0f\n",
             pr[4], pr[5], pr[0] / nl, pr[1] / nl, pr[2] / nl, pr[3] / nl);
+    unsigned long long ap[8];
+    cudaMemcpyFromSymbol(ap, g_aqif2_prof, sizeof(ap));
+    const double na = ap[4] ? (double)ap[4] : 1.0;
+    fprintf(stderr, "[pt_prof] aqif2 solves %llu: factor %.0f breakdown %.0f z %.0f gather %.0f cycles\n",
+            ap[4], ap[0] / na, ap[1] / na, ap[2] / na, ap[3] / na);
   }
   for (void* a : h->allocs)
     if (a) cudaFree(a);
@@ -875,6 +880,8 @@ extern "C" int paqif_ehl_point_get(paqif_ehl_point* h, double* u, double* film, 
   cudaError_t e = cudaStreamSynchronize(st);
   return e == cudaSuccess ? PAQIF_OK : set_cuda_error("ehl_point_get", e);
 }
+
+extern "C" void* paqif_ehl_point_stream(paqif_ehl_point* h) { return h ? (void*)h->st : nullptr; }
 
 extern "C" int paqif_ehl_point_sync(paqif_ehl_point* h) {
   if (!h) return set_arg_error("ehl_point_sync");

@@ -53,6 +53,8 @@ def _bind(L):
     L.paqif_ehl_point_step.restype = ctypes.c_int
     L.paqif_ehl_point_get.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.paqif_ehl_point_get.restype = ctypes.c_int
+    L.paqif_ehl_point_stream.argtypes = [vp]
+    L.paqif_ehl_point_stream.restype = vp
     L.paqif_ehl_point_sync.argtypes = [vp]
     L.paqif_ehl_point_sync.restype = ctypes.c_int
     L.paqif_ehl_point_sweep.argtypes = [vp, i32, i32, i32, f64, u32]
@@ -205,6 +207,10 @@ class PointContact:
         """complementarity_residual of the resident state (synchronises)."""
         _native.check(self.L.paqif_ehl_point_residual(self._h.ptr), "paqif_ehl_point_residual")
         return self.status()[1]
+
+    def stream_handle(self) -> int:
+        """The handle's cudaStream_t (e.g. for torch.cuda.ExternalStream)."""
+        return int(self.L.paqif_ehl_point_stream(self._h.ptr) or 0)
 
     def sync(self) -> None:
         _native.check(self.L.paqif_ehl_point_sync(self._h.ptr), "paqif_ehl_point_sync")
