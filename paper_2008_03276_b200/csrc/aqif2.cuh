@@ -42,15 +42,6 @@ __device__ __forceinline__ double band2_at(const double* __restrict__ band, int 
   return in ? band[(d + 2) * n + i] : 0.0;
 }
 
-// |v| inside (2^-500, 2^500) on the exponent field (integer pipe), the range
-// where the Markstein quotient below is the IEEE quotient (div_rn)
-__device__ __forceinline__ bool exp_safe(double v) {
-  const unsigned e = ((unsigned)__double2hiint(v) >> 20) & 0x7ffu;
-  return e - 524u < 999u;  // 524 <= e <= 1522
-}
-__device__ __forceinline__ bool is_zero(double v) {
-  return ((unsigned)__double2hiint(v) & 0x7fffffffu) == 0u && __double2loint(v) == 0;
-}
 __device__ __forceinline__ double qdiv_rn(double a, double b, double y, bool b_safe) {
   if (b_safe && (exp_safe(a) || is_zero(a))) {
     const double q = __dmul_rn(a, y);
@@ -58,37 +49,6 @@ __device__ __forceinline__ double qdiv_rn(double a, double b, double y, bool b_s
     return fma(r, y, q);
   }
   return __ddiv_rn(a, b);
-}
-// Branch-free quotient for the hot loops: the Markstein value, plus a flag
-// that is false when (a, b) leave the range where it equals a/b.  A branch
-// on a just-computed value costs ~40 cycles on the level recurrence
-// (tools/thr2.cu), so the solver runs this path and repeats the whole solve
-// with qdiv_rn in the (practically never seen) unsafe case.
-__device__ __forceinline__ double mdiv(double a, double b, double y, bool& safe) {
-  // Tiny numerators (the anti-band fill decays through the subnormal range
-  // over a few hundred levels) are scaled by 2^600 first; the scaled
-  // quotient qs = RN(as/b) comes back by 2^-600, which is exact unless the
-  // result is subnormal, where it is a second rounding: that one can only
-  // go wrong when qs sits exactly on a midpoint of the subnormal grid, and
-  // then the exact remainder r = as - b*qs says which side the true
-  // quotient lies on (one subnormal ulp correction).
-  const unsigned ea = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
-  const bool tiny = ea < 524u;
-  const double up = tiny ? 0x1p600 : 1.0, dn = tiny ? 0x1p-600 : 1.0;
-  const double as = a * up;
-  const double q = __dmul_rn(as, y);
-  const double r0 = fma(-q, b, as);
-  const double qs = fma(r0, y, q);
-  const double r = fma(-qs, b, as);  // exact remainder of qs
-  const double res0 = qs * dn;
-  const double back = res0 * up;     // exact
-  const double d = qs - back;        // exact; +-2^-475 on a midpoint
-  const bool tie = fabs(d) == 0x1p-475;
-  const bool pos = (__double2hiint(r) ^ __double2hiint(b)) >= 0;  // sign of r/b
-  const bool rz = is_zero(r);
-  const bool fix = tie && !rz && ((d > 0.0) == pos);
-  safe = safe && (exp_safe(as) || is_zero(a));
-  return fix ? res0 + (d > 0.0 ? 0x1p-1074 : -0x1p-1074) : res0;  // keeps the sign of zero
 }
 template <bool EXACT, bool CHECKED>
 __device__ __forceinline__ double level_div(double a, double b, double y, bool b_safe, bool& safe) {

@@ -21,6 +21,8 @@ template <int BETA>
 struct DropinPol {
   static constexpr bool kFuseW = false;
   static constexpr bool kResidual = true;
+  static constexpr bool kFastDiv = false;  // branch-free divisions, checked repeat
+  static constexpr bool kLazyBreakdown = false;  // breakdown found after the loop
   static constexpr bool kRecordW = true;
   static constexpr int BP1 = BETA + 1;
   double* band;

@@ -14,6 +14,8 @@ constexpr int kLineBeta = 2;
 struct LineSysPol {
   static constexpr bool kFuseW = true;
   static constexpr bool kResidual = false;
+  static constexpr bool kFastDiv = false;  // branch-free divisions, checked repeat
+  static constexpr bool kLazyBreakdown = false;  // breakdown found after the loop
   static constexpr bool kRecordW = false;
   using PL = PivotLayout<kLineBeta>;
   const double* band;

@@ -33,6 +33,8 @@ template <int BETA>
 struct LcpPol {
   static constexpr bool kFuseW = true;
   static constexpr bool kResidual = false;
+  static constexpr bool kFastDiv = true;  // branch-free divisions, checked repeat
+  static constexpr bool kLazyBreakdown = true;  // breakdown found after the loop
   static constexpr bool kRecordW = false;
   using PL = PivotLayout<BETA>;
   const double* band;
@@ -55,10 +57,16 @@ struct LcpPol {
   __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
     double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
     const double2* src = reinterpret_cast<const double2*>(pb);
-    for (int idx = gl; idx < PL::kSize / 2; idx += G) dst[idx] = src[idx];
+    constexpr int NP = PL::kSize / 2, GG = Group<BETA>::G;
+#pragma unroll
+    for (int t = 0; t < (NP + GG - 1) / GG; ++t) {  // straight-line, predicated
+      const int idx = gl + t * G;
+      if (idx < NP) dst[idx] = src[idx];
+    }
   }
   __device__ __forceinline__ void on_w(int, int, double, double) {}
   __device__ __forceinline__ void on_resid(int, int, double) {}
+  __device__ __forceinline__ const double* record(int k) const { return zs + (size_t)k * PL::kSize; }
 };
 
 __device__ __forceinline__ double fmax_(double a, double b) { return b > a ? b : a; }
@@ -200,7 +208,7 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
 }
 
 template <int BETA, bool EXACT, bool SOLVE_ONLY>
-__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 4)
+__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 2)
 lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
            double tol, int max_outer, double* u_out, uint8_t* act_out, int64_t* passes_out,
            double* res_out, int64_t* status_out, char* ws, size_t ws_per_slot, int total_warps)
@@ -279,7 +287,16 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       pol.use_act = !SOLVE_ONLY;
       if (active) passes = outer + 1;
       PAQIF_TSTAMP(t0);
-      if (aqif_factor_group<BETA, EXACT>(pol, n, 1e-14, my_sm.eng, gl, active)) {
+      int fst = aqif_factor_group<BETA, EXACT>(pol, n, 1e-14, my_sm.eng, gl, active);
+      if (EXACT && __any_sync(FULL, fst < 0)) {
+        // a multiplier left the branch-free division's range: repeat this
+        // system's factorization with IEEE divisions (the others idle)
+        __syncwarp();
+        const int f2 = aqif_factor_group<BETA, EXACT, LcpPol<BETA>, false>(
+            pol, n, 1e-14, my_sm.eng, gl, active && fst < 0);
+        if (fst < 0) fst = f2;
+      }
+      if (fst) {
         st = PAQIF_LCP_FACTOR_BREAKDOWN;
         active = false;
       }

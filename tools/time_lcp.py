@@ -20,3 +20,12 @@ for exact in (True, False):
     print(f"exact={exact} B={B} ms={ms:.3f} rows/s={B*1025/(ms*1e-3):.3e} "
           f"GB/s={B*155800/(ms*1e-3)/1e9:.1f} passes_mean={s.passes.double().mean().item():.3f} "
           f"status_max={int(s.status.max())} ws_MB={s.ws_bytes/1e6:.0f}", flush=True)
+    pa = s.passes.cpu().numpy()
+    print("  passes histogram", dict(zip(*np.unique(pa, return_counts=True))), flush=True)
+    for bb in (64, 512, 1024, 2048):
+        sb = LcpSolver(bb, 1026, 8, exact)
+        sb.launch(tb[:bb], tf[:bb]); torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3): sb.launch(tb[:bb], tf[:bb])
+        e1.record(); torch.cuda.synchronize()
+        print(f"  B={bb}: {e0.elapsed_time(e1)/3:.3f} ms, max passes {int(sb.passes.max())}", flush=True)
