@@ -127,3 +127,19 @@ def test_solve_r1_matches_oracle():
     xo, sto = O.paqif_solve_r1_batch(bands, f, threads=8)
     assert np.array_equal(st, sto)
     assert np.array_equal(_bits(x), _bits(xo))
+
+
+def test_lcp_full_config2_fma_matches_exact():
+    """The bench headline runs FMA arithmetic: on all 4096 config-2 systems it
+    takes the same passes and ends in the same active sets as the exact
+    (bit-exact vs the oracle) arithmetic, values within 1e-9 relative."""
+    from paper_2008_03276_b200.batch import lcp_batch
+    from paper_2008_03276_b200.workloads import lcp_batch as gen
+    bands, f = gen(2024, 4096)
+    re_ = lcp_batch(bands, f, exact=True)
+    rf = lcp_batch(bands, f, exact=False)
+    assert np.array_equal(re_.passes, rf.passes)
+    assert np.array_equal(re_.active, rf.active)
+    assert np.all(rf.status == 0)
+    scale = np.maximum(1.0, np.max(np.abs(re_.u), axis=1, keepdims=True))
+    assert np.max(np.abs(rf.u - re_.u) / scale) <= 1e-9
