@@ -99,6 +99,32 @@ int paqif_solve_r1_batch(int64_t B, int64_t n, int64_t beta, const double *bands
                          size_t workspace_bytes, void *stream);
 
 /* Workspace needed by paqif_lcp_batch / paqif_solve_r1_batch for (B, n, beta). */
+/* r-block partitioned PAQIF, all seven steps on the device (paqif_solve,
+ * parallel.py:106-295): B systems of order n = r*t (t even, t > 2 beta),
+ * beta <= 16.  bands [dev] (B, 2beta+1, n), f [dev] (B, n), x [dev] (B, n)
+ * out; project != 0 clamps corners and middles at zero (the LCP pass);
+ * status [dev] (B,) PAQIF_LCP_* (factor / z-solve breakdown, reduced system
+ * not SPD).  The reduced system (order 2 beta r) is solved through its
+ * normal equations with a banded Cholesky; rounding differs from the
+ * reference's numpy/LAPACK there. */
+size_t paqif_solve_rblock_workspace_bytes(int64_t B, int64_t n, int64_t beta, int64_t r);
+int paqif_solve_rblock_batch(int64_t B, int64_t n, int64_t beta, int64_t r,
+                             const double *bands, const double *f, double *x, int32_t project,
+                             int64_t *status, uint32_t flags, void *workspace,
+                             size_t workspace_bytes, void *stream);
+
+/* Active-set pass helpers for paqif_solve_lcp with r > 1 (parallel.py:
+ * 312-343), batched, [dev] pointers.  _pin: lmod/fmod of the active rows
+ * (diagonal kept, 1 if zero; right side 0).  _pass: lam = L u_eval - f,
+ * u = max(u_eval, 0), res[b] = max|min(u, L u - f)|, new_active = u_eval < lam,
+ * changed[b] = new_active differs from active. */
+int paqif_lcp_pin_batch(int64_t B, int64_t n, int64_t beta, const double *bands, const double *f,
+                        const uint8_t *active, double *lmod, double *fmod, void *stream);
+int paqif_lcp_pass_batch(int64_t B, int64_t n, int64_t beta, const double *bands,
+                         const double *f, const double *u_eval, const uint8_t *active,
+                         double *u, uint8_t *new_active, double *res, int32_t *changed,
+                         void *stream);
+
 size_t paqif_lcp_workspace_bytes(int64_t B, int64_t n, int64_t beta);
 
 /* Fused batched projected LCP: u >= 0, L u >= f, u.(L u - f) = 0 for every

@@ -79,6 +79,14 @@ def load(build_if_missing: bool = False):
                                   _vp, _vp, _vp, _sz, _vp]
     L.paqif_lcp_batch_host.argtypes = [_i64, _i64, _i64, _vp, _vp, _f64, _i64, _u32, _vp, _vp,
                                        _vp, _vp, _vp]
+    if hasattr(L, "paqif_solve_rblock_batch"):
+        L.paqif_solve_rblock_workspace_bytes.argtypes = [_i64, _i64, _i64, _i64]
+        L.paqif_solve_rblock_workspace_bytes.restype = _sz
+        L.paqif_solve_rblock_batch.argtypes = [_i64, _i64, _i64, _i64, _vp, _vp, _vp,
+                                               ctypes.c_int32, _vp, _u32, _vp, _sz, _vp]
+        L.paqif_lcp_pin_batch.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.paqif_lcp_pass_batch.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                           _vp, _vp]
     if hasattr(L, "paqif_ehl_line_step"):
         L.paqif_ehl_line_workspace_bytes.argtypes = [_i64, _i64]
         L.paqif_ehl_line_workspace_bytes.restype = _sz

@@ -130,3 +130,99 @@ def solve_r1_batch(bands, f, exact: bool = True):
         torch.cuda.current_stream().synchronize()
         return x.cpu().numpy(), st.cpu().numpy()
     return x, st
+
+
+def _dev(a, dtype=None):
+    torch = _native.torch_cuda()
+    if isinstance(a, np.ndarray):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype or np.float64)).cuda(), True
+    return a.contiguous(), False
+
+
+def solve_rblock_batch(bands, f, r: int, project: bool = False, exact: bool = True,
+                       stream=None):
+    """Batched paqif_solve(L_b, f_b, r) with all seven steps on the device
+    (csrc/rblock.cu).  Returns (x, status) like the inputs (numpy or torch)."""
+    torch = _native.torch_cuda()
+    L = _native.lib()
+    tb, host = _dev(bands)
+    tf, _ = _dev(f)
+    B, beta, n = _shape(tb, tf)
+    nbytes = L.paqif_solve_rblock_workspace_bytes(B, n, beta, r)
+    if nbytes == 0:
+        raise ContractViolationError(f"r-block solve: unsupported sizes n={n} beta={beta} r={r}")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    x = torch.zeros((B, n), dtype=torch.float64, device="cuda")
+    st = torch.zeros(B, dtype=torch.int64, device="cuda")
+    rc = L.paqif_solve_rblock_batch(B, n, beta, int(r), tb.data_ptr(), tf.data_ptr(),
+                                    x.data_ptr(), 1 if project else 0, st.data_ptr(),
+                                    _native.FLAG_EXACT if exact else 0, ws.data_ptr(), nbytes,
+                                    _native.stream_ptr(stream))
+    _native.check(rc, "paqif_solve_rblock_batch")
+    if host:
+        torch.cuda.current_stream().synchronize()
+        return x.cpu().numpy(), st.cpu().numpy()
+    return x, st
+
+
+def lcp_rblock(bands, f, r: int, tol: float = 1e-10, max_outer: int = 100, exact: bool = True):
+    """paqif_solve_lcp(LcpProblem(L, f), r) for r > 1 on the device for one
+    system (parallel.py:298-347): every pass pins the active rows, runs the
+    r-block solve and the multiplier / projection / residual / next-set
+    kernels; the host only reads (res, changed) per pass.  Returns
+    (u, status, passes, res) with status a PAQIF_LCP_* code."""
+    torch = _native.torch_cuda()
+    L = _native.lib()
+    bands = np.ascontiguousarray(bands, dtype=np.float64)
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    nd, n = bands.shape
+    beta = (nd - 1) // 2
+    tb = torch.from_numpy(bands[None]).cuda()
+    tf = torch.from_numpy(f[None]).cuda()
+    scale = float(np.abs(bands).sum(axis=0).max() + np.abs(f).max())
+    floor = 1e3 * np.finfo(float).eps * scale
+    act = (tf <= 0.0).to(torch.uint8)
+    nact = torch.empty_like(act)
+    lmod = torch.empty_like(tb)
+    fmod = torch.empty_like(tf)
+    u = torch.empty_like(tf)
+    res = torch.empty(1, dtype=torch.float64, device="cuda")
+    chg = torch.empty(1, dtype=torch.int32, device="cuda")
+    nbytes = L.paqif_solve_rblock_workspace_bytes(1, n, beta, r)
+    if nbytes == 0:
+        raise ContractViolationError(f"r-block solve: unsupported sizes n={n} beta={beta} r={r}")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ue = torch.zeros_like(tf)
+    st = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sp = _native.stream_ptr()
+    best_res, best_u = np.inf, np.zeros(n)
+    last = np.inf
+    for k in range(max_outer):
+        _native.check(L.paqif_lcp_pin_batch(1, n, beta, tb.data_ptr(), tf.data_ptr(),
+                                             act.data_ptr(), lmod.data_ptr(), fmod.data_ptr(), sp),
+                      "paqif_lcp_pin_batch")
+        _native.check(L.paqif_solve_rblock_batch(1, n, beta, int(r), lmod.data_ptr(),
+                                                 fmod.data_ptr(), ue.data_ptr(), 0, st.data_ptr(),
+                                                 _native.FLAG_EXACT if exact else 0,
+                                                 ws.data_ptr(), nbytes, sp),
+                      "paqif_solve_rblock_batch")
+        _native.check(L.paqif_lcp_pass_batch(1, n, beta, tb.data_ptr(), tf.data_ptr(),
+                                              ue.data_ptr(), act.data_ptr(), u.data_ptr(),
+                                              nact.data_ptr(), res.data_ptr(), chg.data_ptr(), sp),
+                      "paqif_lcp_pass_batch")
+        code = int(st.item())
+        if code:
+            return u[0].cpu().numpy(), code, k + 1, float("nan")
+        last = float(res.item())
+        if last <= tol:
+            return u[0].cpu().numpy(), 0, k + 1, last
+        if last < best_res:
+            best_res, best_u = last, u[0].cpu().numpy()
+        if not int(chg.item()):
+            if best_res <= max(tol, floor):
+                return best_u, 0, k + 1, best_res
+            break
+        act, nact = nact, act
+    if best_res <= max(tol, floor):
+        return best_u, 0, max_outer, best_res
+    return best_u, _native.LCP_NONCONVERGED, max_outer, last

@@ -192,3 +192,74 @@ class TestLcpApi:
         l = BandedMatrix.from_diagonals(4, {0: -1.0, 1: 0.0, -1: 0.0})
         with pytest.raises(ContractViolationError):
             psor_oracle(LcpProblem(l, np.ones(4)))
+
+
+class TestRblockDevice:
+    """paqif_solve(r > 1) runs all seven steps on the device (csrc/rblock.cu)."""
+
+    @pytest.mark.parametrize("n,beta,r", [(96, 2, 4), (256, 3, 8), (1026, 8, 27), (512, 8, 8),
+                                          (640, 12, 10), (64, 1, 16)])
+    def test_batch_vs_dense(self, n, beta, r):
+        from paper_2008_03276_b200.batch import solve_rblock_batch
+        from paper_2008_03276_b200.workloads import lcp_batch as gen
+        bands, f = gen(7 + n, 12, n=n, beta=beta)
+        x, st = solve_rblock_batch(bands, f, r)
+        assert np.all(st == 0)
+        from paper_2008_03276_b200 import BandedMatrix
+        for b in range(bands.shape[0]):
+            l = BandedMatrix(n, beta, bands[b])
+            ud = np.linalg.solve(l.to_dense(), f[b])
+            assert np.max(np.abs(x[b] - ud)) <= 1e-12 * max(1.0, np.max(np.abs(ud)))
+
+    def test_project_flag(self, rng):
+        """project=True against the host restatement of the seven steps
+        (parallel.py's step functions: numpy reduced system, projection of
+        the corners, middles from the projected corners, projection)."""
+        from paper_2008_03276_b200 import BandedMatrix, parallel
+        from paper_2008_03276_b200.batch import solve_rblock_batch
+        from paper_2008_03276_b200.bandcore import project_nonneg
+        from paper_2008_03276_b200.workloads import lcp_batch as gen
+        n, beta, r = 128, 2, 4
+        bands, f = gen(3, 4, n=n, beta=beta)
+        x1, st = solve_rblock_batch(bands, f, r, project=True)
+        assert np.all(st == 0) and np.all(x1 >= 0.0)
+        for b in range(bands.shape[0]):
+            part = parallel.partition(BandedMatrix(n, beta, bands[b]), f[b], r)
+            data = parallel._forward_all(part)
+            ud = project_nonneg(parallel.solve_reduced(parallel.build_reduced_system(part, data)))
+            t = part.block_size
+            bnd = [(ud[2 * beta * m:2 * beta * m + beta], ud[2 * beta * m + beta:2 * beta * (m + 1)])
+                   for m in range(r)]
+            mids = parallel.back_substitute_middle(part, data, bnd)
+            ref = np.concatenate([np.r_[u[:beta], project_nonneg(u[beta:t - beta]), u[t - beta:]]
+                                  for u, _, _ in mids])
+            assert np.max(np.abs(x1[b] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+    def test_statuses(self):
+        from paper_2008_03276_b200.batch import solve_rblock_batch
+        from paper_2008_03276_b200._native import LCP_FACTOR_BREAKDOWN
+        n, beta = 64, 2
+        bands = np.zeros((1, 5, n))
+        bands[0, 2] = 1.0
+        bands[0, 2, 8:24] = 0.0  # singular middle of block 0 of 4 (t = 16)
+        x, st = solve_rblock_batch(bands, np.ones((1, n)), 4)
+        assert int(st[0]) == LCP_FACTOR_BREAKDOWN
+
+    def test_no_host_reduced_system(self, monkeypatch):
+        """The public paqif_solve(r>1) does not touch the host step functions."""
+        from paper_2008_03276_b200 import BandedMatrix, parallel
+        def boom(*a, **k):
+            raise AssertionError("host path used")
+        for name in ("_forward_all", "build_reduced_system", "solve_reduced",
+                     "back_substitute_middle"):
+            monkeypatch.setattr(parallel, name, boom)
+        rng = np.random.default_rng(5)
+        n = 128
+        l = BandedMatrix.from_diagonals(n, {-1: -1.0, 0: 4.0, 1: -1.0})
+        f = rng.standard_normal(n)
+        u = parallel.paqif_solve(l, f, 4)
+        assert np.max(np.abs(u - np.linalg.solve(l.to_dense(), f))) <= 1e-12
+        from paper_2008_03276_b200.lcp import LcpProblem
+        u2 = parallel.paqif_solve_lcp(LcpProblem(l, f), 4, tol=1e-10)
+        u1 = parallel.paqif_solve_lcp(LcpProblem(l, f), 1, tol=1e-10)
+        assert np.max(np.abs(u2 - u1)) <= 1e-10
