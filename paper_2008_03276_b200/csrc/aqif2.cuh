@@ -35,11 +35,39 @@ namespace paqif {
 
 constexpr int kRec2 = 16;
 
-// band: diagonal-major, band[(d + 2) * n + i] = A(i, i + d), |d| <= 2
+// Band storage: diagonal-major with kBandPad zero entries before and after
+// every diagonal (and around the right side), so the level loop reads rows
+// up to 3 outside the matrix without a bounds test:
+//   A(i, i + d) = band[(d + 2) * aqif2_stride(n) + kBandPad + i],  |d| <= 2
+//   f(i)        = rhs[kBandPad + i]
+// Entries whose column leaves the matrix are stored as exact zeros (the
+// padded_bands semantics), so only the row needs the padding.
+constexpr int kBandPad = 4;
+__host__ __device__ constexpr int aqif2_stride(int n) { return n + 2 * kBandPad; }
+__host__ __device__ constexpr size_t aqif2_band_doubles(int n) { return 5 * (size_t)aqif2_stride(n); }
+__host__ __device__ constexpr size_t aqif2_rhs_doubles(int n) { return (size_t)aqif2_stride(n); }
+__device__ __forceinline__ double& band2_ref(double* band, int n, int i, int d) {
+  return band[(d + 2) * aqif2_stride(n) + kBandPad + i];
+}
+// checked access (setup only): zero outside the matrix and the band
 __device__ __forceinline__ double band2_at(const double* __restrict__ band, int n, int i, int j) {
   const int d = j - i;
   const bool in = (unsigned)i < (unsigned)n && (unsigned)j < (unsigned)n && d >= -2 && d <= 2;
-  return in ? band[(d + 2) * n + i] : 0.0;
+  return in ? band[(d + 2) * aqif2_stride(n) + kBandPad + i] : 0.0;
+}
+// unchecked access: |j - i| <= 2 and -kBandPad <= i < n + kBandPad
+__device__ __forceinline__ double band2_pad(const double* __restrict__ band, int n, int i, int j) {
+  return band[(j - i + 2) * aqif2_stride(n) + kBandPad + i];
+}
+// zero the pads of a band + right side (all threads of the CTA call)
+__device__ __forceinline__ void aqif2_zero_pads(double* band, double* rhs, int n) {
+  const int S = aqif2_stride(n);
+  for (int idx = threadIdx.x; idx < 6 * 2 * kBandPad; idx += blockDim.x) {
+    const int row = idx / (2 * kBandPad), q = idx % (2 * kBandPad);
+    const int col = q < kBandPad ? q : kBandPad + n + (q - kBandPad);
+    if (row < 5) band[row * S + col] = 0.0;
+    else rhs[col] = 0.0;
+  }
 }
 
 __device__ __forceinline__ double qdiv_rn(double a, double b, double y, bool b_safe) {
@@ -85,7 +113,7 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
       wo[e] = band2_at(band, n, row, pr + e * dir);
       wc[e] = band2_at(band, n, row, other - e * dir);
     }
-    rh = (unsigned)row < (unsigned)n ? rhs[row] : 0.0;
+    rh = (unsigned)row < (unsigned)n ? rhs[kBandPad + row] : 0.0;
     // level-1 record: the two middle rows (one writer lane per side)
     if (writer && (r & 1) == 0) {
       double* r1 = rec + kRec2;
@@ -94,7 +122,7 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
         r1[own_off + e] = band2_at(band, n, pr, pr + e * dir);
         r1[crs_off + e] = band2_at(band, n, pr, other - e * dir);
       }
-      r1[12 + side] = rhs[pr];
+      r1[12 + side] = rhs[kBandPad + pr];
     }
   }
   __syncwarp();
@@ -103,11 +131,11 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
     const bool nxt = ((r ^ (k - 1)) & 1) == 0;  // my row is the next pivot
     // ---- band loads for the shift at the end of this level
     const int q3 = pr + 3 * dir;                   // row entering the wing
-    const double ncol = band2_at(band, n, row, q3);  // my row's new own column
+    const double ncol = band2_pad(band, n, row, q3);  // my row's new own column
     double fresh[3];
 #pragma unroll
-    for (int e = 0; e < 3; ++e) fresh[e] = band2_at(band, n, q3, pr + dir + e * dir);
-    const double frh = (unsigned)q3 < (unsigned)n ? rhs[q3] : 0.0;
+    for (int e = 0; e < 3; ++e) fresh[e] = band2_pad(band, n, q3, pr + dir + e * dir);
+    const double frh = rhs[kBandPad + q3];
     // ---- this level's pivot rows (record k)
     double* rk = rec + (size_t)k * kRec2;
     double po[3], pc[3], oo[3], oc[3];

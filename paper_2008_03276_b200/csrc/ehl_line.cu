@@ -59,9 +59,11 @@ struct EhlSmemLayout {
     def = o; o += NA;
     red = o; o += 32;
     const int ns = nsys(n);
-    const int sys = 5 * ns + ns + (ns / 2 + 1) * kRec2;
+    const int sys = (int)(aqif2_band_doubles(ns) + aqif2_rhs_doubles(ns)) + (ns / 2 + 1) * kRec2;
     sys_in_smem = (size_t)(o + sys) * 8 <= 227 * 1024;
-    band = o; rhs = o + 5 * ns; rec = rhs + ns;
+    band = o;
+    rhs = o + (int)aqif2_band_doubles(ns);
+    rec = rhs + (int)aqif2_rhs_doubles(ns);
     if (sys_in_smem) o += sys;
     total = o;
   }
@@ -255,8 +257,9 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   // line system: shared memory, or this case's workspace for large n
   double* wsd = reinterpret_cast<double*>(ws + (size_t)b * ws_per_case);
   double* band = L.sys_in_smem ? esm + L.band : wsd;
-  double* rhs = band + (size_t)(2 * kEhlBeta + 1) * n_sys;
-  double* rec = rhs + n_sys;
+  double* rhs = band + aqif2_band_doubles(n_sys);
+  double* rec = rhs + aqif2_rhs_doubles(n_sys);
+  aqif2_zero_pads(band, rhs, n_sys);
   double* xsol = band;  // x overwrites the band after the factor
   const double ph = p_hertz[b], lam = lamv[b];
   const double h = c.h;
@@ -333,9 +336,9 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
         // padded-matrix semantics: rows beyond n_int are identity; entries
         // leaving the (padded) matrix are exact zeros
         const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (d == kEhlBeta);
-        band[(size_t)d * n_sys + r] = keep ? e[d] : 0.0;
+        band2_ref(band, n_sys, r, d - kEhlBeta) = keep ? e[d] : 0.0;
       }
-      rhs[r] = rr;
+      rhs[kBandPad + r] = rr;
     }
     if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
     __syncthreads();
@@ -417,7 +420,8 @@ extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
   const int64_t s = n_sys / 2;
   // the line system lives in shared memory when it fits (EhlSmemLayout)
   if (n <= (1 << 20) && EhlSmemLayout((int)n).sys_in_smem) return (size_t)B * 256;
-  const size_t per = ((size_t)(2 * kEhlBeta + 1) * n_sys + n_sys + (size_t)(s + 1) * kRec2 + 32) * 8;
+  const size_t per = (aqif2_band_doubles((int)n_sys) + aqif2_rhs_doubles((int)n_sys) +
+                      (size_t)(s + 1) * kRec2 + 32) * 8;
   return (size_t)B * ((per + 255) & ~(size_t)255);
 }
 

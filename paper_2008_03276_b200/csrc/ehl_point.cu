@@ -31,7 +31,7 @@ constexpr int kPtThreads = 256;
 constexpr int kLineBeta = 2;
 // line system (5 x n_sys band, right side, AQIF pivot records), doubles
 __host__ __device__ inline size_t pt_sys_doubles(int n_sys) {
-  return (size_t)(2 * kLineBeta + 1) * n_sys + n_sys + (size_t)(n_sys / 2 + 1) * kRec2;
+  return aqif2_band_doubles(n_sys) + aqif2_rhs_doubles(n_sys) + (size_t)(n_sys / 2 + 1) * kRec2;
 }
 constexpr int kMaxPending = 9;
 enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMSize = 24 };
@@ -227,9 +227,9 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
   for (int dd = 0; dd < 5; ++dd) {
     const int col = r + dd - kLineBeta;
     const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (dd == kLineBeta);
-    band[(size_t)dd * n_sys + r] = keep ? e[dd] : 0.0;
+    band2_ref(band, n_sys, r, dd - kLineBeta) = keep ? e[dd] : 0.0;
   }
-  rhs[r] = rr;
+  rhs[kBandPad + r] = rr;
 }
 
 // x-line j of _hybrid_x_sweep (solver.py:91-114) with _line_quantities
@@ -277,8 +277,9 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
     ks1 = s10;
   }
   double* band = sysb;
-  double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
-  double* rec = rhs + n_sys;
+  double* rhs = band + aqif2_band_doubles(n_sys);
+  double* rec = rhs + aqif2_rhs_doubles(n_sys);
+  aqif2_zero_pads(band, rhs, n_sys);
   int rung = 0;
   int st = 1;
   double worst = 0.0;
@@ -435,8 +436,9 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
   const double* t = d.table;
   const double s00 = t[0], s10 = t[N], s01 = t[1], s11 = t[N + 1];
   double* band = sysb;
-  double* rhs = band + (size_t)(2 * kLineBeta + 1) * n_sys;
-  double* rec = rhs + n_sys;
+  double* rhs = band + aqif2_band_doubles(n_sys);
+  double* rec = rhs + aqif2_rhs_doubles(n_sys);
+  aqif2_zero_pads(band, rhs, n_sys);
   int st = 1, rung = 0;
   double worst = 0.0;
   for (; rung < 2; ++rung) {  // 0: tridiagonal system, 1: diagonal fallback

@@ -40,12 +40,14 @@ __global__ void aqif2_kernel(const double* bands, const double* rhss, int n, dou
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
   double* band = sm;
-  double* rhs = band + 5 * n;
-  double* x = rhs + n;
+  double* rhs = band + aqif2_band_doubles(n);
+  double* x = rhs + aqif2_rhs_doubles(n);
   double* rec = x + n;
   __shared__ int flag;
-  for (int i = threadIdx.x; i < 5 * n; i += blockDim.x) band[i] = bands[(size_t)b * 5 * n + i];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) rhs[i] = rhss[(size_t)b * n + i];
+  aqif2_zero_pads(band, rhs, n);
+  for (int i = threadIdx.x; i < 5 * n; i += blockDim.x)
+    band2_ref(band, n, i % n, i / n - 2) = bands[(size_t)b * 5 * n + i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) rhs[kBandPad + i] = rhss[(size_t)b * n + i];
   __syncthreads();
   long long t0 = clock64(), t1 = 0, t2 = 0;
   if (threadIdx.x < 32) {
@@ -119,7 +121,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(db, bands.data(), bands.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dr, rhs.data(), rhs.size() * 8, cudaMemcpyHostToDevice);
   size_t sm1 = sizeof(EngineSmem<2>) + ZChunk<2>::kRing * 8 + 64;
-  size_t sm2 = (size_t)(7 * n + (n / 2 + 1) * kRec2) * 8;
+  size_t sm2 = (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) + n + (size_t)(n / 2 + 1) * kRec2) * 8;
   cudaFuncSetAttribute(aqif2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   cudaFuncSetAttribute(aqif2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   for (int exact = 1; exact >= 0; --exact) {
