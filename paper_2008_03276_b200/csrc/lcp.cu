@@ -211,7 +211,8 @@ template <int BETA, bool EXACT, bool SOLVE_ONLY>
 __global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 2)
 lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
            double tol, int max_outer, double* u_out, uint8_t* act_out, int64_t* passes_out,
-           double* res_out, int64_t* status_out, char* ws, size_t ws_per_slot, int total_warps)
+           double* res_out, int64_t* status_out, char* ws, size_t ws_per_slot, int total_warps,
+           unsigned long long* next_pair)
 {
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
@@ -239,7 +240,10 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
   unsigned long long ph_acc[4] = {0, 0, 0, 0};
 #endif
 
-  for (int64_t base = (int64_t)gw * P; base < B; base += (int64_t)total_warps * P) {
+  // pairs of systems: the first per warp static, then taken from a global
+  // counter as warps finish (pass counts differ per system)
+  int64_t pair = gw;
+  for (int64_t base = pair * P; base < B; base = pair * P) {
     const int64_t b = base + g;
     const bool have = b < B;
     const double* bd = bands + (have ? b : 0) * nb;
@@ -407,6 +411,9 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       if (res_out) res_out[b] = res;
       status_out[b] = st;
     }
+    unsigned long long nx = 0;
+    if (lane == 0) nx = atomicAdd(next_pair, 1ull);
+    pair = total_warps + (int64_t)__shfl_sync(FULL, nx, 0);
   }
 }
 
@@ -414,6 +421,8 @@ template <int BETA>
 constexpr size_t lcp_smem_bytes() {
   return sizeof(LcpSmem<BETA>) * kLcpWarpsPerBlock * Group<BETA>::P;
 }
+
+constexpr size_t kLcpWsHead = 256;  // work counter of the persistent grid
 
 template <int BETA>
 size_t lcp_ws_per_slot(int n) {
@@ -470,15 +479,17 @@ template <int BETA, bool EXACT, bool SOLVE_ONLY>
 int run_lcp(const LcpDispatch& a) {
   const int warps = lcp_grid_warps<BETA, EXACT, SOLVE_ONLY>(a.B);
   const size_t per = lcp_ws_per_slot<BETA>(a.n);
-  const size_t need = per * (size_t)warps * Group<BETA>::P;
+  const size_t need = kLcpWsHead + per * (size_t)warps * Group<BETA>::P;
   if (a.ws_bytes < need) {
     std::snprintf(last_error_buf(), 512, "workspace too small: need %zu bytes", need);
     return PAQIF_E_WORKSPACE;
   }
   const unsigned grid = (unsigned)((warps + kLcpWarpsPerBlock - 1) / kLcpWarpsPerBlock);
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(a.ws);
+  cudaMemsetAsync(counter, 0, sizeof(unsigned long long), a.st);
   lcp_kernel<BETA, EXACT, SOLVE_ONLY><<<grid, 32 * kLcpWarpsPerBlock, lcp_smem_bytes<BETA>(), a.st>>>(
       a.B, a.n, a.bands, a.f, a.tol, a.max_outer, a.u, a.act, a.passes, a.res, a.status,
-      (char*)a.ws, per, warps);
+      (char*)a.ws + kLcpWsHead, per, warps, counter);
   return check_launch("lcp_kernel");
 }
 
@@ -534,7 +545,7 @@ size_t ws_bytes_for(int64_t B, int64_t n, int64_t beta, bool exact) {
     PAQIF_WS_CASE2(8)
 #undef PAQIF_WS_CASE2
   }
-  return per * (size_t)(warps > w2 ? warps : w2);
+  return kLcpWsHead + per * (size_t)(warps > w2 ? warps : w2);
 }
 
 int check_lcp_args(int64_t B, int64_t n, int64_t beta) {
