@@ -82,7 +82,7 @@ template <bool EXACT, bool CHECKED>
 __device__ __forceinline__ double level_div(double a, double b, double y, bool b_safe, bool& safe) {
   if (!EXACT) return a * y;
   if (CHECKED) return qdiv_rn(a, b, y, b_safe);
-  return mdiv(a, b, y, safe);
+  return mdiv_fix(a, b, y, safe);
 }
 
 // Factor + fused W solve.  ALL 32 lanes of one converged warp call (a
