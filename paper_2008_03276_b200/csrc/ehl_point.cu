@@ -628,6 +628,8 @@ using namespace paqif;
 struct paqif_ehl_point {
   paqif_ehl_point_cfg cfg;
   PointDev d;
+  // FFT period: the next power of two >= 2n (exact on the central window for
+  // any pressure, fft_deform.cuh)
   FftPlan plan;
   cudaStream_t st;
   std::vector<void*> allocs;
@@ -647,6 +649,28 @@ T* dalloc(paqif_ehl_point* h, size_t count) {
 
 void fold(paqif_ehl_point* h) {
   fft_deformation(h->plan, h->d.u, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount], h->st);
+}
+
+int next_pow2(int v) {
+  int P = 32;
+  while (P < v) P <<= 1;
+  return P;
+}
+
+bool alloc_plan(paqif_ehl_point* h, FftPlan& p, int P) {
+  p.n = h->d.n;
+  p.P = P;
+  p.logP = 0;
+  while ((1 << p.logP) < p.P) ++p.logP;
+  const size_t PP = (size_t)p.P * p.P;
+  p.W = dalloc<double2>(h, PP);
+  p.T = dalloc<double2>(h, PP);
+  p.KT = dalloc<double2>(h, PP);
+  p.tw = dalloc<double2>(h, p.P / 2 + 1);
+  if (!p.W || !p.T || !p.KT || !p.tw) return false;
+  fft_prepare(p.P);
+  fft_plan_kernel(p, h->d.table, h->st);
+  return true;
 }
 
 }  // namespace
@@ -688,31 +712,24 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.prof = nullptr;
   if (const char* e = getenv("PAQIF_PT_PROF"))
     if (e[0] == '1') d.prof = dalloc<unsigned long long>(h, 8);
-  FftPlan& p = h->plan;
-  p.n = n;
-  p.P = fft_size_for(n);
-  p.logP = 0;
-  while ((1 << p.logP) < p.P) ++p.logP;
-  const size_t PP = (size_t)p.P * p.P;
-  p.W = dalloc<double2>(h, PP);
-  p.T = dalloc<double2>(h, PP);
-  p.KT = dalloc<double2>(h, PP);
-  p.tw = dalloc<double2>(h, p.P / 2 + 1);
   for (void* a : h->allocs)
     if (!a) {
       paqif_ehl_point_destroy(h);
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != (d.prof ? 18u : 17u)) {
+  if (h->allocs.size() != (d.prof ? 14u : 13u)) {
     paqif_ehl_point_destroy(h);
     set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
     return nullptr;
   }
   cudaMemcpyAsync(d.table, table, NN * 8, cudaMemcpyHostToDevice, h->st);
   cudaMemcpyAsync(d.geom, geometry, NN * 8, cudaMemcpyHostToDevice, h->st);
-  fft_prepare(p.P);
-  fft_plan_kernel(p, d.table, h->st);
+  if (!alloc_plan(h, h->plan, next_pow2(2 * n))) {
+    paqif_ehl_point_destroy(h);
+    set_cuda_error("ehl_point: FFT plan", cudaErrorMemoryAllocation);
+    return nullptr;
+  }
   h->line_smem = sizeof(PtShared) + (d.sys_in_smem ? sys_bytes : 0);
   if (cudaStreamSynchronize(h->st) != cudaSuccess || check_launch("ehl_point_create")) {
     paqif_ehl_point_destroy(h);

@@ -5,15 +5,20 @@
 //   D[j][i] = sum_{j',i'} t[|j-j'|][|i-i'|] u[j'][i']      (t symmetric)
 //
 // is the central (n+1)^2 window of the linear convolution of u with the
-// mirrored (2n+1)^2 kernel; a circular convolution of period P >= 2n+1 is
-// alias-free on that window, so P is the next power of two >= 2n+1.
+// mirrored (2n+1)^2 kernel K[c] = t[|c-n|], c = 0..2n.  In a circular
+// convolution of period P the window needs K at offsets c = m - j in
+// [0, 2n] only; for P >= 2n those never wrap except c = 2n -> 0, where
+// K[2n] = K[0] = t[n].  So P = 2n is exact on the window; the driver uses the
+// next power of two >= 2n.
 // Pipeline (complex fp64, radix-2 in shared memory, one CTA per row):
 //   pack u -> row FFT (rows < N) -> transpose -> row FFT (all P)
 //   -> multiply by the transposed kernel spectrum -> inverse row FFT
 //   -> transpose -> inverse row FFT (rows n..2n only) -> extract / P^2.
 // Every kernel takes a device `gate`: with *gate == 0 it returns at once,
 // so the sweep drivers can enqueue the fold pipeline after every line and
-// let the device decide (film.py:83-91 fold rule).
+// let the device decide (film.py:83-91 fold rule).  Grids are capped
+// (grid-stride loops), so a gated-off pipeline costs a few microseconds
+// even at P = 4096 (an uncapped elementwise grid there is 65536 blocks).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -48,8 +53,8 @@ __global__ void fft_rows_kernel(double2* data, int P, int logP, int row0, int ro
                                 const double2* __restrict__ tw, int inverse, const int* gate) {
   if (gate && *gate == 0) return;
   extern __shared__ double2 fsm[];
-  const int r = row0 + blockIdx.x;
-  if (blockIdx.x >= rows) return;
+  for (int rr = blockIdx.x; rr < rows; rr += gridDim.x) {
+  const int r = row0 + rr;
   double2* row = data + (size_t)r * P;
   for (int k = threadIdx.x; k < P; k += blockDim.x) {
     const int rev = __brev(k) >> (32 - logP);
@@ -72,42 +77,50 @@ __global__ void fft_rows_kernel(double2* data, int P, int logP, int row0, int ro
     __syncthreads();
   }
   for (int k = threadIdx.x; k < P; k += blockDim.x) row[k] = fsm[k];
+  __syncthreads();
+  }
 }
 
 __global__ void transpose_kernel(const double2* __restrict__ in, double2* __restrict__ out, int P,
                                  const int* gate) {
   if (gate && *gate == 0) return;
   __shared__ double2 tile[32][33];
-  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int y = threadIdx.y; y < 32; y += blockDim.y)
-    tile[y][threadIdx.x] = in[(size_t)(by + y) * P + bx + threadIdx.x];
-  __syncthreads();
-  for (int y = threadIdx.y; y < 32; y += blockDim.y)
-    out[(size_t)(bx + y) * P + by + threadIdx.x] = tile[threadIdx.x][y];
+  const int tiles_x = P / 32, tiles = tiles_x * tiles_x;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int bx = (t % tiles_x) * 32, by = (t / tiles_x) * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y)
+      tile[y][threadIdx.x] = in[(size_t)(by + y) * P + bx + threadIdx.x];
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y)
+      out[(size_t)(bx + y) * P + by + threadIdx.x] = tile[threadIdx.x][y];
+    __syncthreads();
+  }
 }
 
 // W[r][c] = u[r][c] (r, c < N), else 0; or, for the kernel, the mirrored table
 __global__ void pack_kernel(double2* W, int P, int n, const double* __restrict__ src,
                             int mirrored_table, const int* gate) {
   if (gate && *gate == 0) return;
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)P * P) return;
-  const int r = (int)(idx / P), c = (int)(idx % P);
   const int N = n + 1;
-  double v = 0.0;
-  if (!mirrored_table) {
-    if (r < N && c < N) v = src[(size_t)r * N + c];
-  } else {
-    if (r <= 2 * n && c <= 2 * n) v = src[(size_t)abs(r - n) * N + abs(c - n)];
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)P * P;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / P), c = (int)(idx % P);
+    double v = 0.0;
+    if (!mirrored_table) {
+      if (r < N && c < N) v = src[(size_t)r * N + c];
+    } else {
+      if (r <= 2 * n && c <= 2 * n) v = src[(size_t)abs(r - n) * N + abs(c - n)];
+    }
+    W[idx] = make_double2(v, 0.0);
   }
-  W[idx] = make_double2(v, 0.0);
 }
 
 __global__ void cmul_kernel(double2* T, const double2* __restrict__ K, size_t count,
                             const int* gate) {
   if (gate && *gate == 0) return;
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < count) T[idx] = cmul(T[idx], K[idx]);
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < count;
+       idx += (size_t)gridDim.x * blockDim.x)
+    T[idx] = cmul(T[idx], K[idx]);
 }
 
 // D[j][i] = Re W[j+n][i+n] / P^2; clears the gate (and the pending count)
@@ -115,11 +128,12 @@ __global__ void extract_kernel(const double2* __restrict__ W, int P, int n, doub
                                int* pending_count) {
   if (gate && *gate == 0) return;
   const int N = n + 1;
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double scale = 1.0 / ((double)P * (double)P);
-  if (idx < (size_t)N * N) {
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)N * N;
+       idx += (size_t)gridDim.x * blockDim.x) {
     const int j = (int)(idx / N), i = (int)(idx % N);
-    D[idx] = W[(size_t)(j + n) * P + (i + n)].x * scale;
+    const int rj = j + n < P ? j + n : j + n - P, ci = i + n < P ? i + n : i + n - P;
+    D[idx] = W[(size_t)rj * P + ci].x * scale;
   }
 }
 
@@ -131,16 +145,31 @@ __global__ void gate_clear_kernel(int* gate, int* pending_count) {
 }
 
 inline int fft_threads(int P) { return P >= 1024 ? 512 : (P >= 256 ? 256 : 128); }
+// capped grids: elementwise / transpose tiles / FFT rows
+constexpr unsigned kFftEwBlocks = 148 * 8;
+inline unsigned ew_grid(size_t count) {
+  const size_t b = (count + 255) / 256;
+  return (unsigned)(b < kFftEwBlocks ? (b ? b : 1) : kFftEwBlocks);
+}
+inline unsigned row_grid(int rows, int P) {
+  const int cap = P >= 4096 ? 148 * 3 : 148 * 6;
+  return (unsigned)(rows < cap ? rows : cap);
+}
+inline unsigned tile_grid(int P) {
+  const int tiles = (P / 32) * (P / 32);
+  return (unsigned)(tiles < 148 * 8 ? tiles : 148 * 8);
+}
 
 // Forward transform of the packed W: rows [0, nz_rows) nonzero; result in T
 // (transposed spectrum).
 inline void fft2_forward(const FftPlan& p, int nz_rows, const int* gate, cudaStream_t st) {
   const size_t smem = (size_t)p.P * sizeof(double2);
-  fft_rows_kernel<<<nz_rows, fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, 0, nz_rows, p.tw, 0,
-                                                          gate);
-  dim3 tb(32, 8), tg(p.P / 32, p.P / 32);
-  transpose_kernel<<<tg, tb, 0, st>>>(p.W, p.T, p.P, gate);
-  fft_rows_kernel<<<p.P, fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P, p.tw, 0, gate);
+  fft_rows_kernel<<<row_grid(nz_rows, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, 0,
+                                                                          nz_rows, p.tw, 0, gate);
+  dim3 tb(32, 8);
+  transpose_kernel<<<tile_grid(p.P), tb, 0, st>>>(p.W, p.T, p.P, gate);
+  fft_rows_kernel<<<row_grid(p.P, p.P), fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P,
+                                                                      p.tw, 0, gate);
 }
 
 // Sets cudaFuncAttributeMaxDynamicSharedMemorySize for the row kernel.
@@ -153,8 +182,10 @@ inline cudaError_t fft_prepare(int P) {
 inline void fft_plan_kernel(const FftPlan& p, const double* table, cudaStream_t st) {
   const size_t PP = (size_t)p.P * p.P;
   fft_twiddles<<<(p.P / 2 + 255) / 256, 256, 0, st>>>(p.tw, p.P);
-  pack_kernel<<<(unsigned)((PP + 255) / 256), 256, 0, st>>>(p.W, p.P, p.n, table, 1, nullptr);
-  fft2_forward(p, 2 * p.n + 1, nullptr, st);
+  pack_kernel<<<ew_grid(PP), 256, 0, st>>>(p.W, p.P, p.n, table, 1, nullptr);
+  // the mirrored table has 2n+1 rows; with P = 2n the row 2n wraps onto row 0,
+  // which holds the same tap t[n] (so P = 2n is exact for the central window)
+  fft2_forward(p, 2 * p.n + 1 < p.P ? 2 * p.n + 1 : p.P, nullptr, st);
   cudaMemcpyAsync(p.KT, p.T, PP * sizeof(double2), cudaMemcpyDeviceToDevice, st);
 }
 
@@ -163,23 +194,24 @@ inline void fft_deformation(const FftPlan& p, const double* u, double* D, int* g
                             int* pending_count, cudaStream_t st) {
   const size_t PP = (size_t)p.P * p.P;
   const int N = p.n + 1;
-  pack_kernel<<<(unsigned)((PP + 255) / 256), 256, 0, st>>>(p.W, p.P, p.n, u, 0, gate);
+  pack_kernel<<<ew_grid(PP), 256, 0, st>>>(p.W, p.P, p.n, u, 0, gate);
   fft2_forward(p, N, gate, st);
-  cmul_kernel<<<(unsigned)((PP + 255) / 256), 256, 0, st>>>(p.T, p.KT, PP, gate);
+  cmul_kernel<<<ew_grid(PP), 256, 0, st>>>(p.T, p.KT, PP, gate);
   const size_t smem = (size_t)p.P * sizeof(double2);
-  fft_rows_kernel<<<p.P, fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P, p.tw, 1, gate);
-  dim3 tb(32, 8), tg(p.P / 32, p.P / 32);
-  transpose_kernel<<<tg, tb, 0, st>>>(p.T, p.W, p.P, gate);
-  fft_rows_kernel<<<N, fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, p.n, N, p.tw, 1, gate);
-  extract_kernel<<<(unsigned)(((size_t)N * N + 255) / 256), 256, 0, st>>>(p.W, p.P, p.n, D, gate,
-                                                                         pending_count);
+  fft_rows_kernel<<<row_grid(p.P, p.P), fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P,
+                                                                      p.tw, 1, gate);
+  dim3 tb(32, 8);
+  transpose_kernel<<<tile_grid(p.P), tb, 0, st>>>(p.T, p.W, p.P, gate);
+  // output rows n..2n; with P = 2n the last one wraps to row 0
+  const int r1 = p.n + N <= p.P ? N : p.P - p.n;
+  fft_rows_kernel<<<row_grid(r1, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, p.n, r1,
+                                                                     p.tw, 1, gate);
+  if (r1 < N)
+    fft_rows_kernel<<<row_grid(N - r1, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, 0,
+                                                                           N - r1, p.tw, 1, gate);
+  extract_kernel<<<ew_grid((size_t)N * N), 256, 0, st>>>(p.W, p.P, p.n, D, gate, pending_count);
   gate_clear_kernel<<<1, 32, 0, st>>>(gate, pending_count);
 }
 
-inline int fft_size_for(int n) {
-  int P = 1;
-  while (P < 2 * n + 1) P <<= 1;
-  return P < 32 ? 32 : P;
-}
 
 }  // namespace paqif
