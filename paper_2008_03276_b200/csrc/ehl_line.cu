@@ -228,7 +228,7 @@ ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restri
   if (threadIdx.x == 0) res_out[b] = cmax / c.h;
 }
 
-template <bool EXACT>
+template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kEhlThreads, 1)
 ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                 const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
@@ -256,7 +256,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   double* red = esm + L.red;
   // line system: shared memory, or this case's workspace for large n
   double* wsd = reinterpret_cast<double*>(ws + (size_t)b * ws_per_case);
-  double* band = L.sys_in_smem ? esm + L.band : wsd;
+  double* band = SMEM ? esm + L.band : wsd;  // SMEM: shared address space known
   double* rhs = band + aqif2_band_doubles(n_sys);
   double* rec = rhs + aqif2_rhs_doubles(n_sys);
   aqif2_zero_pads(band, rhs, n_sys);
@@ -441,12 +441,14 @@ extern "C" int paqif_ehl_line_step(const paqif_ehl_line_cfg* cfg, int64_t B, con
   const size_t per = need / (size_t)B;
   cudaStream_t st = (cudaStream_t)stream;
   if (flags & PAQIF_FLAG_EXACT) {
-    cudaFuncSetAttribute(ehl_line_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ehl_line_kernel<true><<<(unsigned)B, kEhlThreads, smem, st>>>(
+    auto kern = L.sys_in_smem ? ehl_line_kernel<true, true> : ehl_line_kernel<true, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(
         *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
   } else {
-    cudaFuncSetAttribute(ehl_line_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ehl_line_kernel<false><<<(unsigned)B, kEhlThreads, smem, st>>>(
+    auto kern = L.sys_in_smem ? ehl_line_kernel<false, true> : ehl_line_kernel<false, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(
         *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
   }
   return check_launch("paqif_ehl_line_step");

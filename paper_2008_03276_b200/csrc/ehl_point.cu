@@ -234,12 +234,14 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
 
 // x-line j of _hybrid_x_sweep (solver.py:91-114) with _line_quantities
 // (sweeps.py:318-341) and assemble_line_system's point terms (sweeps.py:157-267)
-template <bool EXACT>
+template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int j) {
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
-  double* sysb = d.sys_in_smem ? xsm + sizeof(PtShared) / 8 : d.scratch;
+  // SMEM: the line system in shared memory (address space known to the
+  // compiler -> LDS/STS in the solver's level loops)
+  double* sysb = SMEM ? xsm + sizeof(PtShared) / 8 : d.scratch;
   const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
   const double h = c.h;
   const double* u = d.u;
@@ -409,12 +411,12 @@ __global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
 }
 
 // column i of column_sweep (sweeps.py:437-517)
-template <bool EXACT>
+template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int i) {
   extern __shared__ __align__(16) double ysm[];
   PtShared& S = *reinterpret_cast<PtShared*>(ysm);
-  double* sysb = d.sys_in_smem ? ysm + sizeof(PtShared) / 8 : d.scratch;
+  double* sysb = SMEM ? ysm + sizeof(PtShared) / 8 : d.scratch;
   const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
   const double h = c.h;
   const int lo = i - 2 > 0 ? i - 2 : 0;
@@ -783,10 +785,10 @@ void prepare_attrs(paqif_ehl_point* h) {
   if (done) return;
   (void)h;
   const int smem = 227 * 1024;  // the largest any handle asks for
-  cudaFuncSetAttribute(pt_xline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(pt_xline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(pt_yline_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(pt_yline_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_xline_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_xline_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_yline_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_yline_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   done = true;
 }
 
@@ -801,8 +803,13 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
   for (int j = 1; j < n; ++j) {
     pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(d, 0, j - 1, 3);
-    if (exact) pt_xline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
-    else pt_xline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+    if (d.sys_in_smem) {
+      if (exact) pt_xline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+      else pt_xline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+    } else {
+      if (exact) pt_xline_kernel<true, false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+      else pt_xline_kernel<false, false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
+    }
     fold(h);
   }
   if (ctl.defer != 0) {
@@ -821,8 +828,13 @@ void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
     pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(d, 1, lo, L);
-    if (exact) pt_yline_kernel<true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
-    else pt_yline_kernel<false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+    if (d.sys_in_smem) {
+      if (exact) pt_yline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+      else pt_yline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+    } else {
+      if (exact) pt_yline_kernel<true, false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+      else pt_yline_kernel<false, false><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
+    }
     fold(h);
   }
 }
