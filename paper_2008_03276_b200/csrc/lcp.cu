@@ -331,10 +331,11 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       double r = 0.0;
       int changed = 0;
       if (active) {
-        for (int i = gl; i < n; i += G) {
+        // one row of L x and L max(x, 0) against f (interior rows: all
+        // 2*BETA+1 terms, loads issued first)
+        auto row = [&](int i) {
           double acc1 = 0.0, acc2 = 0.0;
           if (i >= BETA && i < n - BETA) {
-            // interior row: all 2*BETA+1 terms, strided pointer walk
             const double* pa = bd + i;
             const double* px = x + (i - BETA);
             double av[2 * BETA + 1], xv[2 * BETA + 1];
@@ -366,7 +367,15 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
           const uint32_t na = xi < lam ? 1u : 0u;
           nxt[i] = na;
           changed |= (na != cur[i]);
+        };
+        // rows in order (the NaN-propagating max is order independent),
+        // two per step so twice the loads are in flight
+        int i = gl;
+        for (; i + G < n; i += 2 * G) {
+          row(i);
+          row(i + G);
         }
+        if (i < n) row(i);
       }
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) {

@@ -30,18 +30,8 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
   const int q = n - 1 - p;
-  double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
-#pragma unroll
-  for (int t = 0; t < BETA; ++t) {
-    if (!CHECK || p - BETA + t >= 0)
-      acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
-    if (!CHECK || q + 1 + t < n)
-      acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd],
-                        xr[(ph - 1 - t + 2 * BETA) % BETA]);
-  }
-  const double oth = __shfl_xor_sync(pair, acc, 1);
-  const double rt = sd == 0 ? acc : oth;
-  const double rb = sd == 0 ? oth : acc;
+  // the 2x2 pivot, its determinant, reciprocal and breakdown test depend on
+  // the record only: issued first, they run under the right side's chain
   const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
   const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
   const double det = A::det2(a11, a22, a12, a21);
@@ -49,16 +39,47 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
   if (fabs(a12) > scale) scale = fabs(a12);
   if (fabs(a21) > scale) scale = fabs(a21);
   if (fabs(a22) > scale) scale = fabs(a22);
-  if (fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY) return false;
+  const bool bad = fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY;
+  const double y = EXACT ? __drcp_rn(det) : 1.0 / det;
+  double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
   if (EXACT) {
-    const double y = __drcp_rn(det);
+    // reference order: t = 0..BETA-1, left term then right term
+#pragma unroll
+    for (int t = 0; t < BETA; ++t) {
+      if (!CHECK || p - BETA + t >= 0)
+        acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
+      if (!CHECK || q + 1 + t < n)
+        acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd],
+                          xr[(ph - 1 - t + 2 * BETA) % BETA]);
+    }
+  } else {
+    // FMA arithmetic: the terms of the older unknowns first, the two that
+    // the previous level just produced (x[p-1], x[q+1]) last, so only two
+    // FMAs wait on the previous level
+#pragma unroll
+    for (int t = 0; t < BETA; ++t) {
+      if (t != BETA - 1 && (!CHECK || p - BETA + t >= 0))
+        acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
+      if (t != 0 && (!CHECK || q + 1 + t < n))
+        acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd],
+                          xr[(ph - 1 - t + 2 * BETA) % BETA]);
+    }
+    if (!CHECK || q + 1 < n)
+      acc = A::axpy_neg(acc, rec[PL::zi(1, 1, 0) + sd], xr[(ph - 1 + 2 * BETA) % BETA]);
+    if (!CHECK || p - 1 >= 0)
+      acc = A::axpy_neg(acc, rec[PL::zi(0, 1, 0) + sd], xl[(ph + BETA - 1) % BETA]);
+  }
+  const double oth = __shfl_xor_sync(pair, acc, 1);
+  const double rt = sd == 0 ? acc : oth;
+  const double rb = sd == 0 ? oth : acc;
+  if (bad) return false;
+  if (EXACT) {
     const bool ds = div_safe(det);
     xp = div_rn(A::det2(a22, rt, a12, rb), det, y, ds);
     xq = div_rn(A::det2(a11, rb, a21, rt), det, y, ds);
   } else {
-    const double inv = 1.0 / det;
-    xp = (a22 * rt - a12 * rb) * inv;
-    xq = (a11 * rb - a21 * rt) * inv;
+    xp = (a22 * rt - a12 * rb) * y;
+    xq = (a11 * rb - a21 * rt) * y;
   }
   return true;
 }
