@@ -40,7 +40,7 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
   if (fabs(a21) > scale) scale = fabs(a21);
   if (fabs(a22) > scale) scale = fabs(a22);
   const bool bad = fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY;
-  const double y = EXACT ? __drcp_rn(det) : 1.0 / det;
+  const double y = __drcp_rn(det);  // RN(1/det), either arithmetic
   double acc = rec[sd == 0 ? PL::kYT : PL::kYB];
   if (EXACT) {
     // reference order: t = 0..BETA-1, left term then right term
