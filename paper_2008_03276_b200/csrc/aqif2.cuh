@@ -163,11 +163,11 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
     const double nm = A::det2(oc[0], wo[0], oo[0], wc[0]);
     const double no = A::det2(po[0], wc[0], pc[0], wo[0]);
     const bool ds = exp_safe(det);
-    safe = safe && ds;
+    safe = safe & ds;
     const double wm = level_div<EXACT, CHECKED>(nm, det, y, ds, safe);
     const double wx = level_div<EXACT, CHECKED>(no, det, y, ds, safe);
     const bool ok = (unsigned)row < (unsigned)n;
-    const bool up = ok && !(is_zero(wm) && is_zero(wx));
+    const bool up = ok & !(is_zero(wm) & is_zero(wx));  // bitwise: no branches
     const double u1 = A::rank2(wo[1], wm, po[1], wx, oo[1]);
     const double u2 = A::rank2(wo[2], wm, po[2], wx, oo[2]);
     const double v1 = A::rank2(wc[1], wm, pc[1], wx, oc[1]);
@@ -183,7 +183,7 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
     rh = ok ? rr : rh;
     // ---- next pivot: publish as record k+1, then take the entering row
     double* rn = rk + kRec2;
-    if (writer && nxt) {
+    if (writer & nxt) {
 #pragma unroll
       for (int e = 0; e < 3; ++e) {
         rn[own_off + e] = wo[e];
@@ -245,7 +245,7 @@ __device__ bool aqif2_zsolve(double* rec_, int n, int lane_id) {
     const double a11 = c[0], a12 = c[3], a21 = c[6], a22 = c[9];
     const double det = c[14], y = c[15];
     const bool ds = exp_safe(det);
-    safe = safe && ds;
+    safe = safe & ds;
     const double xp = level_div<EXACT, CHECKED>(A::det2(a22, at, a12, ab), det, y, ds, safe);
     const double xq = level_div<EXACT, CHECKED>(A::det2(a11, ab, a21, at), det, y, ds, safe);
     if (lane_id == 0) {  // the record's y_t, y_b were read above (same warp instruction stream)
