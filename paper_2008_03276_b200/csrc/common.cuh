@@ -75,7 +75,7 @@ __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     double w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = (v != v || w != w) ? __longlong_as_double(0x7ff8000000000000ll) : (w > v ? w : v);
+    v = ((v != v) | (w != w)) ? __longlong_as_double(0x7ff8000000000000ll) : (w > v ? w : v);
   }
   return v;
 }

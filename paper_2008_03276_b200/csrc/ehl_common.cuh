@@ -15,10 +15,10 @@ constexpr double kSwitch = 0.6;
 // ---------------------------------------------------------------- limiters
 // tvdcd.limiter_psi / limiter_weight_plus (tvdcd.py:207-235)
 __device__ __forceinline__ double np_maximum(double a, double b) {
-  return (a >= b || a != a) ? a : b;
+  return ((a >= b) | (a != a)) ? a : b;
 }
 __device__ __forceinline__ double np_minimum(double a, double b) {
-  return (a <= b || a != a) ? a : b;
+  return ((a <= b) | (a != a)) ? a : b;
 }
 static __device__ double limiter_psi(double r, int name, double kappa) {
   switch (name) {
@@ -64,7 +64,7 @@ static __device__ double block_nanmax(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = (v != v || w != w) ? qnan : (w > v ? w : v);
+    v = ((v != v) | (w != w)) ? qnan : (w > v ? w : v);
   }
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -72,7 +72,7 @@ static __device__ double block_nanmax(double v, double* red) {
   double r = red[0];
   for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
     const double x = red[w];
-    r = (r != r || x != x) ? qnan : (x > r ? x : r);
+    r = ((r != r) | (x != x)) ? qnan : (x > r ? x : r);
   }
   __syncthreads();
   return r;

@@ -196,7 +196,7 @@ __device__ double line_comp_residual(const paqif_ehl_line_cfg& c, double h0, con
       r = (e_p * (sun[i + 1] - sun[i]) + e_m * (sun[i - 1] - sun[i])) / h - fd;
     }
     const double m = fabs(np_minimum(sun[i], -r));
-    comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+    comp = ((comp != comp) | (m != m)) ? qnan : (m > comp ? m : comp);
   }
   return block_nanmax(comp, red);
 }

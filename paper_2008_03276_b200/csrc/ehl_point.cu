@@ -604,12 +604,12 @@ __global__ void pt_residual_kernel(PointDev d, paqif_ehl_point_cfg c) {
             h * fd;
       }
       const double m = fabs(np_minimum(d.u[(size_t)j * N + i], -r));
-      comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+      comp = ((comp != comp) | (m != m)) ? qnan : (m > comp ? m : comp);
     }
   } else {
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const double m = fabs(np_minimum(d.u[(size_t)j * N + i], -0.0));
-      comp = (comp != comp || m != m) ? qnan : (m > comp ? m : comp);
+      comp = ((comp != comp) | (m != m)) ? qnan : (m > comp ? m : comp);
     }
   }
   const double cm = block_nanmax(comp, red);

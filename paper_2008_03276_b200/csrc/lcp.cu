@@ -72,9 +72,9 @@ struct LcpPol {
 __device__ __forceinline__ double fmax_(double a, double b) { return b > a ? b : a; }
 
 // numpy maximum(x, 0.0) / minimum(a, b) semantics (NaN propagating, -0.0 kept)
-__device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
+__device__ __forceinline__ double np_max0(double x) { return ((x >= 0.0) | (x != x)) ? x : 0.0; }
 __device__ __forceinline__ double np_min(double a, double b) {
-  return (a <= b || a != a) ? a : b;
+  return ((a <= b) | (a != a)) ? a : b;
 }
 
 constexpr int kLcpWarpsPerBlock = 4;
@@ -363,7 +363,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
           const double lam = A::sub(acc1, fb[i]);
           const double rr = A::sub(acc2, fb[i]);
           const double mn = fabs(np_min(np_max0(xi), rr));
-          r = (r != r || mn != mn) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
+          r = ((r != r) | (mn != mn)) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
           const uint32_t na = xi < lam ? 1u : 0u;
           nxt[i] = na;
           changed |= (na != cur[i]);
@@ -380,7 +380,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) {
         const double w = __shfl_xor_sync(FULL, r, o);
-        r = (r != r || w != w) ? __longlong_as_double(0x7ff8000000000000ll) : (w > r ? w : r);
+        r = ((r != r) | (w != w)) ? __longlong_as_double(0x7ff8000000000000ll) : (w > r ? w : r);
         changed |= __shfl_xor_sync(FULL, changed, o);
       }
       PAQIF_TSTAMP(t4);

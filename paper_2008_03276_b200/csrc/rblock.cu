@@ -431,7 +431,7 @@ __global__ void lcp_pass_kernel(int n, int beta, const double* __restrict__ band
     const double lam = le - f[(size_t)b * n + i];
     const double r = lu - f[(size_t)b * n + i];
     const double mn = fabs((xu[i] <= r || xu[i] != xu[i]) ? xu[i] : r);
-    m = (m != m || mn != mn) ? qnan : (mn > m ? mn : m);
+    m = ((m != m) | (mn != mn)) ? qnan : (mn > m ? mn : m);
     const uint8_t na = xe[i] < lam ? 1 : 0;
     c |= na != act[(size_t)b * n + i];
     nact[(size_t)b * n + i] = na;
@@ -440,7 +440,7 @@ __global__ void lcp_pass_kernel(int n, int beta, const double* __restrict__ band
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double w2 = __shfl_xor_sync(0xffffffffu, m, o);
-    m = (m != m || w2 != w2) ? qnan : (w2 > m ? w2 : m);
+    m = ((m != m) | (w2 != w2)) ? qnan : (w2 > m ? w2 : m);
   }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -448,7 +448,7 @@ __global__ void lcp_pass_kernel(int n, int beta, const double* __restrict__ band
     double r = red[0];
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
       const double x2 = red[k];
-      r = (r != r || x2 != x2) ? qnan : (x2 > r ? x2 : r);
+      r = ((r != r) | (x2 != x2)) ? qnan : (x2 > r ? x2 : r);
     }
     res[b] = r;
     changed[b] = chg;
