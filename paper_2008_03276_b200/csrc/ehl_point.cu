@@ -61,6 +61,7 @@ struct PointDev {
   int32_t* xinfo;   // n-1: newton tag | rung << 4
   int32_t* yinfo;   // n-1: rung
   double* film_out; // N x N
+  double* rcache;   // 8 x N: rheology (eps, rho) of the points a line reads
 };
 
 __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_ehl_point_cfg& c,
@@ -251,11 +252,20 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
   auto eps_at = [&](int r, int i, double& rho) {
     return rheo_eps(u[(size_t)r * N + i], film(r, i), c, rho);
   };
-  // pass 1: min(eps_line)/h and max|q_line|
+  // pass 1: rheology of rows j-1, j, j+1 once (cached: eps rows 0..2, rho
+  // of row j), min(eps_line)/h and max|q_line|
+  double* E0 = d.rcache;
+  double* E1 = E0 + N;
+  double* E2 = E1 + N;
+  double* R1 = E2 + N;
   double emin = INFINITY, qmax = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double rho;
+    double rho, rdum;
     const double e = eps_at(j, i, rho);
+    E1[i] = e;
+    R1[i] = rho;
+    E0[i] = eps_at(j - 1, i, rdum);
+    E2[i] = eps_at(j + 1, i, rdum);
     emin = fmin(emin, e);
     qmax = fmax(qmax, fabs(rho * film(j, i)));
   }
@@ -291,18 +301,12 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
       double rr = 0.0;
       if (r < n_int) {
         const int i = r + 1;
-        double rw, rc, re, rdum, rm2 = 0.0;
-        const double ew = eps_at(j, i - 1, rw);
-        const double ec = eps_at(j, i, rc);
-        const double ee = eps_at(j, i + 1, re);
-        const double es = eps_at(j - 1, i, rdum);
-        const double en = eps_at(j + 1, i, rdum);
+        const double rw = R1[i - 1], rc = R1[i], re = R1[i + 1];
+        const double ew = E1[i - 1], ec = E1[i], ee = E1[i + 1];
+        const double es = E0[i], en = E2[i];
         const double qw = rw * film(j, i - 1), qc = rc * film(j, i), qe = re * film(j, i + 1);
         double qww = 0.0;
-        if (i >= 2) {
-          eps_at(j, i - 2, rm2);
-          qww = rm2 * film(j, i - 2);
-        }
+        if (i >= 2) qww = R1[i - 2] * film(j, i - 2);
         const double dqi = qe - qc, dqm = qc - qw;
         const double php = limiter_wplus(gratio(dqi, dqm, gfloor), c.limiter, c.kappa);
         const double phm = i >= 2 ? limiter_wplus(gratio(dqm, qw - qww, gfloor), c.limiter, c.kappa)
@@ -427,11 +431,15 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
   auto eps_at = [&](int l, int m, double& rho) {
     return rheo_eps(u[(size_t)m * N + (lo + l)], film(l, m), c, rho);
   };
+  // rheology of the bundle's L columns once (cached), max|q| over them
+  double* EC = d.rcache;          // [l][m] eps
+  double* RC = d.rcache + 4 * N;  // [l][m] rho
   double qmax = 0.0;
   for (int k = threadIdx.x; k < L * N; k += blockDim.x) {
     const int l = k / N, m = k % N;
     double rho;
-    eps_at(l, m, rho);
+    EC[k] = eps_at(l, m, rho);
+    RC[k] = rho;
     qmax = fmax(qmax, fabs(rho * film(l, m)));
   }
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
@@ -449,12 +457,11 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
       double rr = 0.0;
       if (r < n_int) {
         const int jj = r + 1;
-        double rc, rw, re, rdum, rww = 0.0;
-        const double ec = eps_at(pos, jj, rc);
-        const double ew = eps_at(pos - 1, jj, rw);
-        const double ee = eps_at(pos + 1, jj, re);
-        const double es = eps_at(pos, jj - 1, rdum);
-        const double en = eps_at(pos, jj + 1, rdum);
+        auto ce = [&](int l, int m) { return EC[(size_t)l * N + m]; };
+        auto cr = [&](int l, int m) { return RC[(size_t)l * N + m]; };
+        const double rc = cr(pos, jj), rw = cr(pos - 1, jj), re = cr(pos + 1, jj);
+        const double ec = ce(pos, jj), ew = ce(pos - 1, jj), ee = ce(pos + 1, jj);
+        const double es = ce(pos, jj - 1), en = ce(pos, jj + 1);
         const double ey_p = 0.5 * (ec + en) * h, ey_m = 0.5 * (ec + es) * h;
         const double ex_p = 0.5 * (ec + ee) * h, ex_m = 0.5 * (ec + ew) * h;
         const double qc = rc * film(pos, jj), qw = rw * film(pos - 1, jj), qe = re * film(pos + 1, jj);
@@ -462,8 +469,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
         const double php = limiter_wplus(gratio(dq_p, dq_m, gfloor), c.limiter, c.kappa);
         double phm = 0.0;
         if (pos >= 2) {
-          eps_at(pos - 2, jj, rww);
-          const double qww = rww * film(pos - 2, jj);
+          const double qww = cr(pos - 2, jj) * film(pos - 2, jj);
           phm = limiter_wplus(gratio(dq_m, qw - qww, gfloor), c.limiter, c.kappa);
         }
         const double flux_p = qc + 0.5 * php * dq_p;
@@ -711,6 +717,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.xinfo = dalloc<int32_t>(h, N);
   d.yinfo = dalloc<int32_t>(h, N);
   d.film_out = dalloc<double>(h, NN);
+  d.rcache = dalloc<double>(h, 8 * (size_t)N);
   d.prof = nullptr;
   if (const char* e = getenv("PAQIF_PT_PROF"))
     if (e[0] == '1') d.prof = dalloc<unsigned long long>(h, 8);
@@ -720,7 +727,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != (d.prof ? 14u : 13u)) {
+  if (h->allocs.size() != (d.prof ? 15u : 14u)) {
     paqif_ehl_point_destroy(h);
     set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
     return nullptr;
