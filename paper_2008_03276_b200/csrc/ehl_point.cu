@@ -89,18 +89,30 @@ __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_eh
 // thread per output.  Launch: kPtFilmWarps warps per block, enough blocks
 // for L*N warps.
 constexpr int kPtFilmWarps = 8;
-__global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d, int mode,
-                                                                     int first, int L) {
+__global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
+                                                                     paqif_ehl_point_cfg c,
+                                                                     int mode, int first, int L) {
   const int N = d.N;
   const int count = d.meta[kMCount];
   const double h0 = d.scal[0];
+  auto gidx = [&](int line, int idx) {
+    return mode == 0 ? (size_t)line * N + idx : (size_t)idx * N + line;
+  };
   auto base = [&](int line, int idx) {
-    const size_t g = mode == 0 ? (size_t)line * N + idx : (size_t)idx * N + line;
+    const size_t g = gidx(line, idx);
     return (h0 + d.geom[g]) + d.dbase[g];
+  };
+  // film value o plus its rheology (eps, rho) for the line kernel: the
+  // pointwise work of a line spread over the whole GPU
+  auto emit = [&](int o, int line, int idx, double v) {
+    d.films[o] = v;
+    double rho;
+    d.rcache[o] = rheo_eps(d.u[gidx(line, idx)], v, c, rho);
+    d.rcache[4 * (size_t)N + o] = rho;
   };
   if (count == 0) {
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
-    if (o < L * N) d.films[o] = base(first + o / N, o % N);
+    if (o < L * N) emit(o, first + o / N, o % N, base(first + o / N, o % N));
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -131,7 +143,7 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
     for (int off = 16; off > 0; off >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, off);
     corr += sp;
   }
-  if (lane == 0) d.films[o] = base(line, idx) + corr;
+  if (lane == 0) emit(o, line, idx, base(line, idx) + corr);
 }
 
 __device__ __forceinline__ double block_min(double v, double* red) {
@@ -252,22 +264,16 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
   auto eps_at = [&](int r, int i, double& rho) {
     return rheo_eps(u[(size_t)r * N + i], film(r, i), c, rho);
   };
-  // pass 1: rheology of rows j-1, j, j+1 once (cached: eps rows 0..2, rho
-  // of row j), min(eps_line)/h and max|q_line|
-  double* E0 = d.rcache;
-  double* E1 = E0 + N;
-  double* E2 = E1 + N;
-  double* R1 = E2 + N;
+  // pass 1: the rheology of rows j-1, j, j+1 came with the films
+  // (pt_films_kernel); min(eps_line)/h and max|q_line|
+  const double* E0 = d.rcache;
+  const double* E1 = E0 + N;
+  const double* E2 = E1 + N;
+  const double* R1 = d.rcache + 4 * (size_t)N + N;
   double emin = INFINITY, qmax = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double rho, rdum;
-    const double e = eps_at(j, i, rho);
-    E1[i] = e;
-    R1[i] = rho;
-    E0[i] = eps_at(j - 1, i, rdum);
-    E2[i] = eps_at(j + 1, i, rdum);
-    emin = fmin(emin, e);
-    qmax = fmax(qmax, fabs(rho * film(j, i)));
+    emin = fmin(emin, E1[i]);
+    qmax = fmax(qmax, fabs(R1[i] * film(j, i)));
   }
   const double ratio = block_min(emin, S.red) / h;
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
@@ -431,16 +437,13 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
   auto eps_at = [&](int l, int m, double& rho) {
     return rheo_eps(u[(size_t)m * N + (lo + l)], film(l, m), c, rho);
   };
-  // rheology of the bundle's L columns once (cached), max|q| over them
-  double* EC = d.rcache;          // [l][m] eps
-  double* RC = d.rcache + 4 * N;  // [l][m] rho
+  // the rheology of the bundle's L columns came with the films
+  const double* EC = d.rcache;          // [l][m] eps
+  const double* RC = d.rcache + 4 * N;  // [l][m] rho
   double qmax = 0.0;
   for (int k = threadIdx.x; k < L * N; k += blockDim.x) {
     const int l = k / N, m = k % N;
-    double rho;
-    EC[k] = eps_at(l, m, rho);
-    RC[k] = rho;
-    qmax = fmax(qmax, fabs(rho * film(l, m)));
+    qmax = fmax(qmax, fabs(RC[k] * film(l, m)));
   }
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
   const double* t = d.table;
@@ -809,7 +812,7 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   cudaMemsetAsync(d.sigma, 0, NN * 8, st);
   cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
   for (int j = 1; j < n; ++j) {
-    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(d, 0, j - 1, 3);
+    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(d, h->cfg, 0, j - 1, 3);
     if (d.sys_in_smem) {
       if (exact) pt_xline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
       else pt_xline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
@@ -834,7 +837,7 @@ void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   for (int i = 1; i < n; ++i) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
-    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(d, 1, lo, L);
+    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(d, h->cfg, 1, lo, L);
     if (d.sys_in_smem) {
       if (exact) pt_yline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
       else pt_yline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
