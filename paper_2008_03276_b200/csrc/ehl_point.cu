@@ -659,7 +659,8 @@ T* dalloc(paqif_ehl_point* h, size_t count) {
 }
 
 void fold(paqif_ehl_point* h) {
-  fft_deformation(h->plan, h->d.u, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount], h->st);
+  // one cooperative launch; a no-op (gate == 0) costs one empty kernel
+  fft_fold(h->plan, h->d.u, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount], h->st);
 }
 
 int next_pow2(int v) {

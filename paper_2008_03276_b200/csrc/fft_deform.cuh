@@ -20,6 +20,7 @@
 // (grid-stride loops), so a gated-off pipeline costs a few microseconds
 // even at P = 4096 (an uncapped elementwise grid there is 65536 blocks).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace paqif {
@@ -144,7 +145,126 @@ __global__ void gate_clear_kernel(int* gate, int* pending_count) {
   }
 }
 
+// one radix-2 FFT of a row of P complex values through shared memory (fsm)
+__device__ __forceinline__ void fft_row_smem(double2* row, int P, int logP,
+                                             const double2* __restrict__ tw, int inverse,
+                                             double2* fsm) {
+  for (int k = threadIdx.x; k < P; k += blockDim.x) fsm[__brev(k) >> (32 - logP)] = row[k];
+  __syncthreads();
+  for (int s = 0; s < logP; ++s) {
+    const int m = 1 << s;
+    const int tstride = P >> (s + 1);
+    for (int j = threadIdx.x; j < P / 2; j += blockDim.x) {
+      const int k = j & (m - 1);
+      const int base = (j >> s) << (s + 1);
+      double2 w = tw[k * tstride];
+      if (inverse) w.y = -w.y;
+      const double2 a = fsm[base + k];
+      const double2 b = cmul(fsm[base + k + m], w);
+      fsm[base + k] = make_double2(a.x + b.x, a.y + b.y);
+      fsm[base + k + m] = make_double2(a.x - b.x, a.y - b.y);
+    }
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < P; k += blockDim.x) row[k] = fsm[k];
+  __syncthreads();
+}
+
+// The whole gated fold as ONE cooperative kernel (grid-wide syncs between
+// the phases): a fold that does not fire costs one launch, not ten.
+// Phases as in fft_deformation below.  Dynamic smem: P double2.
+__global__ void fft_fold_kernel(FftPlan p, const double* __restrict__ u, double* D, int* gate,
+                                int* pending_count) {
+  if (*gate == 0) return;  // every block reads the same gate before anyone clears it
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 fsm[];
+  const int P = p.P, n = p.n, N = n + 1;
+  const size_t PP = (size_t)P * P;
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t gthreads = (size_t)gridDim.x * blockDim.x;
+  // pack u into W
+  for (size_t idx = gtid; idx < PP; idx += gthreads) {
+    const int r = (int)(idx / P), c = (int)(idx % P);
+    p.W[idx] = make_double2((r < N && c < N) ? u[(size_t)r * N + c] : 0.0, 0.0);
+  }
+  grid.sync();
+  for (int r = blockIdx.x; r < N; r += gridDim.x) fft_row_smem(p.W + (size_t)r * P, P, p.logP, p.tw, 0, fsm);
+  grid.sync();
+  auto transpose = [&](const double2* in, double2* out) {
+    double2* tile = fsm;  // 32 x 33
+    const int tiles_x = P / 32, tiles = tiles_x * tiles_x;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int bx = (t % tiles_x) * 32, by = (t / tiles_x) * 32;
+      for (int y = ty; y < 32; y += ny) tile[y * 33 + tx] = in[(size_t)(by + y) * P + bx + tx];
+      __syncthreads();
+      for (int y = ty; y < 32; y += ny) out[(size_t)(bx + y) * P + by + tx] = tile[tx * 33 + y];
+      __syncthreads();
+    }
+  };
+  transpose(p.W, p.T);
+  grid.sync();
+  for (int r = blockIdx.x; r < P; r += gridDim.x) fft_row_smem(p.T + (size_t)r * P, P, p.logP, p.tw, 0, fsm);
+  grid.sync();
+  for (size_t idx = gtid; idx < PP; idx += gthreads) p.T[idx] = cmul(p.T[idx], p.KT[idx]);
+  grid.sync();
+  for (int r = blockIdx.x; r < P; r += gridDim.x) fft_row_smem(p.T + (size_t)r * P, P, p.logP, p.tw, 1, fsm);
+  grid.sync();
+  transpose(p.T, p.W);
+  grid.sync();
+  // output rows n..2n (row 2n wraps to row 0 when P = 2n)
+  for (int rr = blockIdx.x; rr < N; rr += gridDim.x) {
+    const int r = n + rr < P ? n + rr : n + rr - P;
+    fft_row_smem(p.W + (size_t)r * P, P, p.logP, p.tw, 1, fsm);
+  }
+  grid.sync();
+  const double scale = 1.0 / ((double)P * (double)P);
+  for (size_t idx = gtid; idx < (size_t)N * N; idx += gthreads) {
+    const int j = (int)(idx / N), i = (int)(idx % N);
+    const int rj = j + n < P ? j + n : j + n - P, ci = i + n < P ? i + n : i + n - P;
+    D[idx] = p.W[(size_t)rj * P + ci].x * scale;
+  }
+  grid.sync();
+  if (gtid == 0) {
+    *gate = 0;
+    if (pending_count) *pending_count = 0;
+  }
+}
+
 inline int fft_threads(int P) { return P >= 1024 ? 512 : (P >= 256 ? 256 : 128); }
+
+// cooperative grid of fft_fold_kernel (blocks resident at once), cached per P
+inline unsigned fold_grid(int P) {
+  static int cachedP = 0;
+  static unsigned g = 0;
+  if (cachedP != P) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)P * sizeof(double2) > 33 * 32 * sizeof(double2)
+                            ? (size_t)P * sizeof(double2) : 33 * 32 * sizeof(double2);
+    cudaFuncSetAttribute(fft_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fft_fold_kernel, fft_threads(P), smem);
+    g = (unsigned)(sms * (per > 0 ? per : 1));
+    cachedP = P;
+  }
+  return g;
+}
+
+inline cudaError_t fft_fold(const FftPlan& p, const double* u, double* D, int* gate,
+                            int* pending_count, cudaStream_t st) {
+  const size_t smem = (size_t)p.P * sizeof(double2) > 33 * 32 * sizeof(double2)
+                          ? (size_t)p.P * sizeof(double2) : 33 * 32 * sizeof(double2);
+  FftPlan pp = p;
+  const double* uu = u;
+  double* dd = D;
+  int* gg = gate;
+  int* pc = pending_count;
+  void* args[] = {&pp, &uu, &dd, &gg, &pc};
+  return cudaLaunchCooperativeKernel((const void*)fft_fold_kernel, dim3(fold_grid(p.P)),
+                                     dim3(fft_threads(p.P)), args, smem, st);
+}
 // capped grids: elementwise / transpose tiles / FFT rows
 constexpr unsigned kFftEwBlocks = 148 * 8;
 inline unsigned ew_grid(size_t count) {
