@@ -603,11 +603,14 @@ extern "C" int paqif_solve_r1_batch(int64_t B, int64_t n, int64_t beta, const do
 namespace {
 // Device staging reused across host-entry calls (grown on demand), so the
 // host path pays for copies and the kernel, not for cudaMalloc each call.
+constexpr int kHostChunksMax = 4;
+
 struct HostStage {
   std::mutex mu;
   char* buf = nullptr;
   size_t cap = 0;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr, st_in = nullptr, st_out = nullptr;
+  cudaEvent_t ev[3][kHostChunksMax] = {};
   int device = -1;
   char* get(size_t bytes) {
     int dev = 0;
@@ -616,10 +619,17 @@ struct HostStage {
       // a different device: the old allocation belongs to another context
       buf = nullptr;
       cap = 0;
-      st = nullptr;
+      st = st_in = st_out = nullptr;
+      for (auto& row : ev)
+        for (auto& e : row) e = nullptr;
       device = dev;
     }
     if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (!st_in && cudaStreamCreateWithFlags(&st_in, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (!st_out && cudaStreamCreateWithFlags(&st_out, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (auto& row : ev)
+      for (auto& e : row)
+        if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
     if (bytes > cap) {
       if (buf) cudaFree(buf);
       buf = nullptr;
@@ -663,21 +673,49 @@ extern "C" int paqif_lcp_batch_host(int64_t B, int64_t n, int64_t beta, const do
   int64_t* d_s = (int64_t*)(base + o_s);
   int rc = PAQIF_OK;
   cudaError_t e;
-  if ((e = cudaMemcpyAsync(d_b, bands, nb * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d_f, f, nv * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    rc = set_cuda_error("lcp_host: h2d", e);
-  if (!rc)
-    rc = paqif_lcp_batch(B, n, beta, d_b, d_f, tol, max_outer, flags, d_u, d_a, d_p, d_r, d_s,
-                         base + o_w, wsb, st);
-  if (!rc) {
-    if ((e = cudaMemcpyAsync(u, d_u, nv * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(active, d_a, nv, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(passes, d_p, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(res, d_r, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(status, d_s, B * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+  // Chunked pipeline: the H2D copy of chunk c+1 (copy stream) overlaps the
+  // solve of chunk c (compute stream), whose D2H overlaps chunk c+1's solve.
+  // The host link, not the solve, bounds this entry point for config 2;
+  // chunks below ~1000 systems would hit the solve's latency floor, so big
+  // batches use up to kHostChunksMax chunks.
+  const int64_t chunks = B >= 2048 ? kHostChunksMax : 1;
+  const int64_t per = (B + chunks - 1) / chunks;
+  const size_t rowb = (size_t)(2 * beta + 1) * n;
+  for (int64_t c = 0; c < chunks && !rc; ++c) {
+    const int64_t b0 = c * per, bc = (b0 + per <= B ? per : B - b0);
+    if (bc <= 0) break;
+    if ((e = cudaMemcpyAsync(d_b + b0 * rowb, bands + b0 * rowb, bc * rowb * 8,
+                             cudaMemcpyHostToDevice, hs.st_in)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(d_f + b0 * n, f + b0 * n, bc * n * 8, cudaMemcpyHostToDevice,
+                             hs.st_in)) != cudaSuccess ||
+        (e = cudaEventRecord(hs.ev[0][c], hs.st_in)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(st, hs.ev[0][c], 0)) != cudaSuccess) {
+      rc = set_cuda_error("lcp_host: h2d", e);
+      break;
+    }
+    rc = paqif_lcp_batch(bc, n, beta, d_b + b0 * rowb, d_f + b0 * n, tol, max_outer, flags,
+                         d_u + b0 * n, d_a + b0 * n, d_p + b0, d_r + b0, d_s + b0, base + o_w,
+                         wsb, st);
+    if (rc) break;
+    if ((e = cudaEventRecord(hs.ev[1][c], st)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(hs.st_out, hs.ev[1][c], 0)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(u + b0 * n, d_u + b0 * n, bc * n * 8, cudaMemcpyDeviceToHost,
+                             hs.st_out)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(active + b0 * n, d_a + b0 * n, bc * n, cudaMemcpyDeviceToHost,
+                             hs.st_out)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(passes + b0, d_p + b0, bc * 8, cudaMemcpyDeviceToHost,
+                             hs.st_out)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(res + b0, d_r + b0, bc * 8, cudaMemcpyDeviceToHost,
+                             hs.st_out)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(status + b0, d_s + b0, bc * 8, cudaMemcpyDeviceToHost,
+                             hs.st_out)) != cudaSuccess)
       rc = set_cuda_error("lcp_host: d2h", e);
   }
-  e = cudaStreamSynchronize(st);
+  cudaError_t e1 = cudaStreamSynchronize(hs.st_in);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  e = cudaStreamSynchronize(hs.st_out);
+  if (!rc && e1 != cudaSuccess) rc = set_cuda_error("lcp_host: sync", e1);
+  if (!rc && e2 != cudaSuccess) rc = set_cuda_error("lcp_host: sync", e2);
   if (!rc && e != cudaSuccess) rc = set_cuda_error("lcp_host: sync", e);
   return rc;
 }
