@@ -674,15 +674,11 @@ bool alloc_plan(paqif_ehl_point* h, FftPlan& p, int P) {
   p.P = P;
   p.logP = 0;
   while ((1 << p.logP) < p.P) ++p.logP;
-  const size_t PP = (size_t)p.P * p.P;
-  p.W = dalloc<double2>(h, PP);
-  p.T = dalloc<double2>(h, PP);
-  p.KT = dalloc<double2>(h, PP);
+  p.W = dalloc<double2>(h, fft_w_elems(p.P));
+  p.KT = dalloc<double2>(h, fft_kt_elems(p.P));
   p.tw = dalloc<double2>(h, p.P / 2 + 1);
-  if (!p.W || !p.T || !p.KT || !p.tw) return false;
-  fft_prepare(p.P);
-  fft_plan_kernel(p, h->d.table, h->st);
-  return true;
+  if (!p.W || !p.KT || !p.tw) return false;
+  return fft_plan_kernel(p, h->d.table, h->st) == cudaSuccess;
 }
 
 }  // namespace

@@ -2,23 +2,32 @@
 // (replaces scipy.fft.rfftn/irfftn in FilmModel.deformation_full,
 // paqif/ehl/film.py:43-56, 72-76).
 //
-//   D[j][i] = sum_{j',i'} t[|j-j'|][|i-i'|] u[j'][i']      (t symmetric)
+//   D[j][i] = sum_{j',i'} t[|j-j'|][|i-i'|] u[j'][i']
 //
 // is the central (n+1)^2 window of the linear convolution of u with the
-// mirrored (2n+1)^2 kernel K[c] = t[|c-n|], c = 0..2n.  In a circular
-// convolution of period P the window needs K at offsets c = m - j in
-// [0, 2n] only; for P >= 2n those never wrap except c = 2n -> 0, where
-// K[2n] = K[0] = t[n].  So P = 2n is exact on the window; the driver uses the
-// next power of two >= 2n.
-// Pipeline (complex fp64, radix-2 in shared memory, one CTA per row):
-//   pack u -> row FFT (rows < N) -> transpose -> row FFT (all P)
-//   -> multiply by the transposed kernel spectrum -> inverse row FFT
-//   -> transpose -> inverse row FFT (rows n..2n only) -> extract / P^2.
-// Every kernel takes a device `gate`: with *gate == 0 it returns at once,
-// so the sweep drivers can enqueue the fold pipeline after every line and
-// let the device decide (film.py:83-91 fold rule).  Grids are capped
-// (grid-stride loops), so a gated-off pipeline costs a few microseconds
-// even at P = 4096 (an uncapped elementwise grid there is 65536 blocks).
+// mirrored (2n+1)^2 kernel K[r][c] = t[|r-n|][|c-n|].  In a circular
+// convolution of period P the window needs K at offsets in [0, 2n] only; for
+// P >= 2n those never wrap except 2n -> 0, where K[2n] = K[0] (= t[n] taps).
+// So P = 2n is exact on the window; the driver uses the next power of two
+// >= 2n.
+//
+// One cooperative kernel, three phases separated by grid barriers; no
+// transposes and no P x P complex buffers:
+//   R  rows r < N: real row of length P packed as H = P/2 complex points
+//      (even + i odd), DIF FFT of length H in shared memory, split into the
+//      H+1 non-redundant bins of the real row's spectrum  -> W[r][0..H]
+//   C  columns k = 0..H: load W[.][k] (rows >= N are zero), DIF FFT of
+//      length P (bit-reversed result), multiply by the kernel spectrum
+//      (stored in the same bit-reversed order), inverse DIT FFT (natural
+//      order), keep the N output rows n..2n (wrapped)   -> W[m][k]
+//   I  output rows m < N: merge bins k and H-k back into H complex points,
+//      inverse DIT FFT of length H, unpack even/odd, scale 1/(P H) -> D[m]
+// The kernel spectrum is made once by phases R and C of the same kernel
+// (plan mode).  Butterflies are radix-2^2 (two radix-2 stages per barrier,
+// 4 points per thread), twiddles staged in shared memory.
+// Every launch takes a device `gate`: with *gate == 0 it returns at once, so
+// the sweep drivers can enqueue a fold after every line and let the device
+// decide (film.py:83-91 fold rule).
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -27,17 +36,27 @@ namespace paqif {
 
 struct FftPlan {
   int n;        // intervals; grid N = n+1
-  int P;        // power of two >= 2n+1
+  int P;        // power of two >= 2n
   int logP;
-  double2* W;   // P*P work
-  double2* T;   // P*P work (transposed)
-  double2* KT;  // P*P transposed kernel spectrum
+  double2* W;   // P rows x (P/2 + 1) bins: half spectra / column results
+  double2* KT;  // (P/2 + 1) columns x P: kernel spectrum, bit-reversed rows
   double2* tw;  // P/2 twiddles exp(-2 pi i t / P)
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 tw_at(const double2* twd, int idx, int inverse) {
+  const double2 w = twd[idx];
+  return inverse ? make_double2(w.x, -w.y) : w;
+}
+__device__ __forceinline__ int bitrev(int k, int bits) { return (int)(__brev(k) >> (32 - bits)); }
 
 __global__ void fft_twiddles(double2* tw, int P) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -48,193 +67,183 @@ __global__ void fft_twiddles(double2* tw, int P) {
   }
 }
 
-// In-place radix-2 FFT of `rows` rows of length P (row stride P), first row
-// `row0`; inverse = conjugated twiddles, unnormalised.
-__global__ void fft_rows_kernel(double2* data, int P, int logP, int row0, int rows,
-                                const double2* __restrict__ tw, int inverse, const int* gate) {
-  if (gate && *gate == 0) return;
-  extern __shared__ double2 fsm[];
-  for (int rr = blockIdx.x; rr < rows; rr += gridDim.x) {
-  const int r = row0 + rr;
-  double2* row = data + (size_t)r * P;
-  for (int k = threadIdx.x; k < P; k += blockDim.x) {
-    const int rev = __brev(k) >> (32 - logP);
-    fsm[rev] = row[k];
+// Decimation in frequency, natural order in -> bit-reversed order out, length
+// L = 2^logL <= Ptw = 2^logPtw (twiddle e^{-2 pi i k / (2m)} = twd[k Ptw/(2m)]).
+// Caller synchronises before; ends synchronised.
+__device__ __forceinline__ void fft_dif_smem(double2* x, int L, int logL, const double2* twd,
+                                             int logPtw, int inverse) {
+  int lm = logL - 1;  // m = 2^lm: current butterfly span
+  for (; lm >= 1; lm -= 2) {
+    const int m = 1 << lm, h = m >> 1;
+    const int sa = logPtw - lm - 1, sb = logPtw - lm;  // twiddle strides (log2)
+    for (int j = threadIdx.x; j < L / 4; j += blockDim.x) {
+      const int q = j & (h - 1);
+      const int base = (j >> (lm - 1)) << (lm + 1);
+      const double2 x0 = x[base + q], x1 = x[base + q + h];
+      const double2 x2 = x[base + q + m], x3 = x[base + q + m + h];
+      const double2 a0 = cadd(x0, x2), a1 = cadd(x1, x3);
+      const double2 a2 = cmul(csub(x0, x2), tw_at(twd, q << sa, inverse));
+      const double2 a3 = cmul(csub(x1, x3), tw_at(twd, (q + h) << sa, inverse));
+      const double2 wb = tw_at(twd, q << sb, inverse);
+      x[base + q] = cadd(a0, a1);
+      x[base + q + h] = cmul(csub(a0, a1), wb);
+      x[base + q + m] = cadd(a2, a3);
+      x[base + q + m + h] = cmul(csub(a2, a3), wb);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int s = 0; s < logP; ++s) {
-    const int m = 1 << s;
-    const int tstride = P >> (s + 1);
-    for (int j = threadIdx.x; j < P / 2; j += blockDim.x) {
+  if (lm == 0) {  // odd log2 L: last span-1 stage, unit twiddles
+    for (int j = threadIdx.x; j < L / 2; j += blockDim.x) {
+      const double2 a = x[2 * j], b = x[2 * j + 1];
+      x[2 * j] = cadd(a, b);
+      x[2 * j + 1] = csub(a, b);
+    }
+    __syncthreads();
+  }
+}
+
+// Decimation in time, bit-reversed order in -> natural order out.
+__device__ __forceinline__ void fft_dit_smem(double2* x, int L, int logL, const double2* twd,
+                                             int logPtw, int inverse) {
+  int s = 0;
+  for (; s + 1 < logL; s += 2) {
+    const int m = 1 << s;  // stage s pairs (q, q+m); stage s+1 pairs (q, q+2m)
+    const int s0 = logPtw - s - 1, s1 = logPtw - s - 2;
+    for (int j = threadIdx.x; j < L / 4; j += blockDim.x) {
+      const int q = j & (m - 1);
+      const int base = (j >> s) << (s + 2);
+      const double2 w0 = tw_at(twd, q << s0, inverse);
+      const double2 x0 = x[base + q], x1 = x[base + q + m];
+      const double2 x2 = x[base + q + 2 * m], x3 = x[base + q + 3 * m];
+      const double2 t1 = cmul(x1, w0), t3 = cmul(x3, w0);
+      const double2 a0 = cadd(x0, t1), a1 = csub(x0, t1);
+      const double2 u2 = cmul(cadd(x2, t3), tw_at(twd, q << s1, inverse));
+      const double2 u3 = cmul(csub(x2, t3), tw_at(twd, (q + m) << s1, inverse));
+      x[base + q] = cadd(a0, u2);
+      x[base + q + 2 * m] = csub(a0, u2);
+      x[base + q + m] = cadd(a1, u3);
+      x[base + q + 3 * m] = csub(a1, u3);
+    }
+    __syncthreads();
+  }
+  if (s < logL) {  // odd log2 L: last radix-2 stage
+    const int m = 1 << s, sh = logPtw - s - 1;
+    for (int j = threadIdx.x; j < L / 2; j += blockDim.x) {
       const int k = j & (m - 1);
       const int base = (j >> s) << (s + 1);
-      double2 w = tw[k * tstride];
-      if (inverse) w.y = -w.y;
-      const double2 a = fsm[base + k];
-      const double2 b = cmul(fsm[base + k + m], w);
-      fsm[base + k] = make_double2(a.x + b.x, a.y + b.y);
-      fsm[base + k + m] = make_double2(a.x - b.x, a.y - b.y);
+      const double2 a = x[base + k];
+      const double2 b = cmul(x[base + k + m], tw_at(twd, k << sh, inverse));
+      x[base + k] = cadd(a, b);
+      x[base + k + m] = csub(a, b);
     }
     __syncthreads();
   }
-  for (int k = threadIdx.x; k < P; k += blockDim.x) row[k] = fsm[k];
-  __syncthreads();
-  }
 }
 
-__global__ void transpose_kernel(const double2* __restrict__ in, double2* __restrict__ out, int P,
-                                 const int* gate) {
-  if (gate && *gate == 0) return;
-  __shared__ double2 tile[32][33];
-  const int tiles_x = P / 32, tiles = tiles_x * tiles_x;
-  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int bx = (t % tiles_x) * 32, by = (t / tiles_x) * 32;
-    for (int y = threadIdx.y; y < 32; y += blockDim.y)
-      tile[y][threadIdx.x] = in[(size_t)(by + y) * P + bx + threadIdx.x];
-    __syncthreads();
-    for (int y = threadIdx.y; y < 32; y += blockDim.y)
-      out[(size_t)(bx + y) * P + by + threadIdx.x] = tile[threadIdx.x][y];
-    __syncthreads();
-  }
-}
-
-// W[r][c] = u[r][c] (r, c < N), else 0; or, for the kernel, the mirrored table
-__global__ void pack_kernel(double2* W, int P, int n, const double* __restrict__ src,
-                            int mirrored_table, const int* gate) {
-  if (gate && *gate == 0) return;
-  const int N = n + 1;
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)P * P;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int r = (int)(idx / P), c = (int)(idx % P);
-    double v = 0.0;
-    if (!mirrored_table) {
-      if (r < N && c < N) v = src[(size_t)r * N + c];
-    } else {
-      if (r <= 2 * n && c <= 2 * n) v = src[(size_t)abs(r - n) * N + abs(c - n)];
-    }
-    W[idx] = make_double2(v, 0.0);
-  }
-}
-
-__global__ void cmul_kernel(double2* T, const double2* __restrict__ K, size_t count,
-                            const int* gate) {
-  if (gate && *gate == 0) return;
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < count;
-       idx += (size_t)gridDim.x * blockDim.x)
-    T[idx] = cmul(T[idx], K[idx]);
-}
-
-// D[j][i] = Re W[j+n][i+n] / P^2; clears the gate (and the pending count)
-__global__ void extract_kernel(const double2* __restrict__ W, int P, int n, double* D, int* gate,
-                               int* pending_count) {
-  if (gate && *gate == 0) return;
-  const int N = n + 1;
-  const double scale = 1.0 / ((double)P * (double)P);
-  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)N * N;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int j = (int)(idx / N), i = (int)(idx % N);
-    const int rj = j + n < P ? j + n : j + n - P, ci = i + n < P ? i + n : i + n - P;
-    D[idx] = W[(size_t)rj * P + ci].x * scale;
-  }
-}
-
-__global__ void gate_clear_kernel(int* gate, int* pending_count) {
-  if (threadIdx.x == 0 && blockIdx.x == 0 && gate && *gate) {
-    *gate = 0;
-    if (pending_count) *pending_count = 0;
-  }
-}
-
-// one radix-2 FFT of a row of P complex values through shared memory (fsm)
-__device__ __forceinline__ void fft_row_smem(double2* row, int P, int logP,
-                                             const double2* __restrict__ tw, int inverse,
-                                             double2* fsm) {
-  for (int k = threadIdx.x; k < P; k += blockDim.x) fsm[__brev(k) >> (32 - logP)] = row[k];
-  __syncthreads();
-  for (int s = 0; s < logP; ++s) {
-    const int m = 1 << s;
-    const int tstride = P >> (s + 1);
-    for (int j = threadIdx.x; j < P / 2; j += blockDim.x) {
-      const int k = j & (m - 1);
-      const int base = (j >> s) << (s + 1);
-      double2 w = tw[k * tstride];
-      if (inverse) w.y = -w.y;
-      const double2 a = fsm[base + k];
-      const double2 b = cmul(fsm[base + k + m], w);
-      fsm[base + k] = make_double2(a.x + b.x, a.y + b.y);
-      fsm[base + k + m] = make_double2(a.x - b.x, a.y - b.y);
-    }
-    __syncthreads();
-  }
-  for (int k = threadIdx.x; k < P; k += blockDim.x) row[k] = fsm[k];
-  __syncthreads();
-}
-
-// The whole gated fold as ONE cooperative kernel (grid-wide syncs between
-// the phases): a fold that does not fire costs one launch, not ten.
-// Phases as in fft_deformation below.  Dynamic smem: P double2.
-__global__ void fft_fold_kernel(FftPlan p, const double* __restrict__ u, double* D, int* gate,
-                                int* pending_count) {
-  if (*gate == 0) return;  // every block reads the same gate before anyone clears it
+// plan_mode 0: D = deformation(src = u, N x N), gated; clears the gate and the
+// pending count.  plan_mode 1: KT = spectrum of the mirrored table (src).
+// Dynamic smem: P + P/2 double2.
+__global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* __restrict__ src,
+                                                       double* D, int* gate, int* pending_count,
+                                                       int plan_mode) {
+  if (gate && *gate == 0) return;  // every block reads the gate before anyone clears it
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double2 fsm[];
-  const int P = p.P, n = p.n, N = n + 1;
-  const size_t PP = (size_t)P * P;
-  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t gthreads = (size_t)gridDim.x * blockDim.x;
-  // pack u into W
-  for (size_t idx = gtid; idx < PP; idx += gthreads) {
-    const int r = (int)(idx / P), c = (int)(idx % P);
-    p.W[idx] = make_double2((r < N && c < N) ? u[(size_t)r * N + c] : 0.0, 0.0);
-  }
-  grid.sync();
-  for (int r = blockIdx.x; r < N; r += gridDim.x) fft_row_smem(p.W + (size_t)r * P, P, p.logP, p.tw, 0, fsm);
-  grid.sync();
-  auto transpose = [&](const double2* in, double2* out) {
-    double2* tile = fsm;  // 32 x 33
-    const int tiles_x = P / 32, tiles = tiles_x * tiles_x;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int bx = (t % tiles_x) * 32, by = (t / tiles_x) * 32;
-      for (int y = ty; y < 32; y += ny) tile[y * 33 + tx] = in[(size_t)(by + y) * P + bx + tx];
-      __syncthreads();
-      for (int y = ty; y < 32; y += ny) out[(size_t)(bx + y) * P + by + tx] = tile[tx * 33 + y];
-      __syncthreads();
+  const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1, n = p.n, N = n + 1;
+  const int ld = H + 1;
+  double2* buf = fsm;
+  double2* twd = fsm + P;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) twd[k] = p.tw[k];
+  const int rows = plan_mode ? (2 * n + 1 < P ? 2 * n + 1 : P) : N;
+
+  // ---- R: half spectra of the real rows
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int c = threadIdx.x; c < H; c += blockDim.x) {
+      const int c0 = 2 * c, c1 = 2 * c + 1;
+      double v0 = 0.0, v1 = 0.0;
+      if (!plan_mode) {
+        const double* row = src + (size_t)r * N;
+        if (c0 < N) v0 = row[c0];
+        if (c1 < N) v1 = row[c1];
+      } else {
+        const double* row = src + (size_t)abs(r - n) * N;
+        if (c0 < rows) v0 = row[abs(c0 - n)];
+        if (c1 < rows) v1 = row[abs(c1 - n)];
+      }
+      buf[c] = make_double2(v0, v1);
     }
-  };
-  transpose(p.W, p.T);
-  grid.sync();
-  for (int r = blockIdx.x; r < P; r += gridDim.x) fft_row_smem(p.T + (size_t)r * P, P, p.logP, p.tw, 0, fsm);
-  grid.sync();
-  for (size_t idx = gtid; idx < PP; idx += gthreads) p.T[idx] = cmul(p.T[idx], p.KT[idx]);
-  grid.sync();
-  for (int r = blockIdx.x; r < P; r += gridDim.x) fft_row_smem(p.T + (size_t)r * P, P, p.logP, p.tw, 1, fsm);
-  grid.sync();
-  transpose(p.T, p.W);
-  grid.sync();
-  // output rows n..2n (row 2n wraps to row 0 when P = 2n)
-  for (int rr = blockIdx.x; rr < N; rr += gridDim.x) {
-    const int r = n + rr < P ? n + rr : n + rr - P;
-    fft_row_smem(p.W + (size_t)r * P, P, p.logP, p.tw, 1, fsm);
+    __syncthreads();
+    fft_dif_smem(buf, H, logH, twd, logP, 0);
+    double2* out = p.W + (size_t)r * ld;
+    for (int k = threadIdx.x; k <= H; k += blockDim.x) {
+      const double2 zk = buf[bitrev(k & (H - 1), logH)];
+      const double2 zm = buf[bitrev((H - k) & (H - 1), logH)];
+      const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+      const double2 o = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+      const double2 w = k < H ? twd[k] : make_double2(-1.0, 0.0);
+      out[k] = cadd(e, cmul(w, o));
+    }
+    __syncthreads();
   }
   grid.sync();
-  const double scale = 1.0 / ((double)P * (double)P);
-  for (size_t idx = gtid; idx < (size_t)N * N; idx += gthreads) {
-    const int j = (int)(idx / N), i = (int)(idx % N);
-    const int rj = j + n < P ? j + n : j + n - P, ci = i + n < P ? i + n : i + n - P;
-    D[idx] = p.W[(size_t)rj * P + ci].x * scale;
+
+  // ---- C: column transforms, kernel product, inverse, output rows
+  for (int k = blockIdx.x; k <= H; k += gridDim.x) {
+    for (int r = threadIdx.x; r < P; r += blockDim.x)
+      buf[r] = r < rows ? p.W[(size_t)r * ld + k] : make_double2(0.0, 0.0);
+    __syncthreads();
+    fft_dif_smem(buf, P, logP, twd, logP, 0);
+    double2* kt = p.KT + (size_t)k * P;
+    if (plan_mode) {
+      for (int j = threadIdx.x; j < P; j += blockDim.x) kt[j] = buf[j];
+      __syncthreads();
+      continue;
+    }
+    for (int j = threadIdx.x; j < P; j += blockDim.x) buf[j] = cmul(buf[j], kt[j]);
+    __syncthreads();
+    fft_dit_smem(buf, P, logP, twd, logP, 1);
+    for (int m = threadIdx.x; m < N; m += blockDim.x) {
+      const int r = m + n < P ? m + n : m + n - P;  // row 2n wraps to 0 when P = 2n
+      p.W[(size_t)m * ld + k] = buf[r];
+    }
+    __syncthreads();
+  }
+  if (plan_mode) return;
+  grid.sync();
+
+  // ---- I: real output rows from their half spectra
+  const double scale = 1.0 / ((double)P * (double)H);
+  for (int m = blockIdx.x; m < N; m += gridDim.x) {
+    const double2* in = p.W + (size_t)m * ld;
+    for (int k = threadIdx.x; k < H; k += blockDim.x) {
+      const double2 yk = in[k], ym = in[H - k];
+      const double2 e = make_double2(0.5 * (yk.x + ym.x), 0.5 * (yk.y - ym.y));
+      const double2 o = cmul(make_double2(0.5 * (yk.x - ym.x), 0.5 * (yk.y + ym.y)),
+                             tw_at(twd, k, 1));
+      buf[bitrev(k, logH)] = make_double2(e.x - o.y, e.y + o.x);
+    }
+    __syncthreads();
+    fft_dit_smem(buf, H, logH, twd, logP, 1);
+    double* out = D + (size_t)m * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const int c = i + n < P ? i + n : i + n - P;
+      const double2 v = buf[c >> 1];
+      out[i] = ((c & 1) ? v.y : v.x) * scale;
+    }
+    __syncthreads();
   }
   grid.sync();
-  if (gtid == 0) {
+  if (gate && blockIdx.x == 0 && threadIdx.x == 0) {
     *gate = 0;
     if (pending_count) *pending_count = 0;
   }
 }
 
-inline int fft_threads(int P) { return P >= 1024 ? 512 : (P >= 256 ? 256 : 128); }
+constexpr int kFftThreads = 256;
+inline size_t fold_smem(int P) { return (size_t)(P + P / 2) * sizeof(double2); }
 
-// cooperative grid of fft_fold_kernel (blocks resident at once), cached per P
+// cooperative grid of fft_conv_kernel (blocks resident at once), cached per P
 inline unsigned fold_grid(int P) {
   static int cachedP = 0;
   static unsigned g = 0;
@@ -242,96 +251,46 @@ inline unsigned fold_grid(int P) {
     int dev = 0, sms = 148, per = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = (size_t)P * sizeof(double2) > 33 * 32 * sizeof(double2)
-                            ? (size_t)P * sizeof(double2) : 33 * 32 * sizeof(double2);
-    cudaFuncSetAttribute(fft_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fft_fold_kernel, fft_threads(P), smem);
+    const size_t smem = fold_smem(P);
+    cudaFuncSetAttribute(fft_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fft_conv_kernel, kFftThreads, smem);
     g = (unsigned)(sms * (per > 0 ? per : 1));
     cachedP = P;
   }
   return g;
 }
 
-inline cudaError_t fft_fold(const FftPlan& p, const double* u, double* D, int* gate,
-                            int* pending_count, cudaStream_t st) {
-  const size_t smem = (size_t)p.P * sizeof(double2) > 33 * 32 * sizeof(double2)
-                          ? (size_t)p.P * sizeof(double2) : 33 * 32 * sizeof(double2);
+inline cudaError_t fft_conv_launch(const FftPlan& p, const double* src, double* D, int* gate,
+                                   int* pending_count, int plan_mode, cudaStream_t st) {
+  const size_t smem = fold_smem(p.P);
   FftPlan pp = p;
-  const double* uu = u;
+  const double* ss = src;
   double* dd = D;
   int* gg = gate;
   int* pc = pending_count;
-  void* args[] = {&pp, &uu, &dd, &gg, &pc};
-  return cudaLaunchCooperativeKernel((const void*)fft_fold_kernel, dim3(fold_grid(p.P)),
-                                     dim3(fft_threads(p.P)), args, smem, st);
-}
-// capped grids: elementwise / transpose tiles / FFT rows
-constexpr unsigned kFftEwBlocks = 148 * 8;
-inline unsigned ew_grid(size_t count) {
-  const size_t b = (count + 255) / 256;
-  return (unsigned)(b < kFftEwBlocks ? (b ? b : 1) : kFftEwBlocks);
-}
-inline unsigned row_grid(int rows, int P) {
-  const int cap = P >= 4096 ? 148 * 3 : 148 * 6;
-  return (unsigned)(rows < cap ? rows : cap);
-}
-inline unsigned tile_grid(int P) {
-  const int tiles = (P / 32) * (P / 32);
-  return (unsigned)(tiles < 148 * 8 ? tiles : 148 * 8);
+  int pm = plan_mode;
+  void* args[] = {&pp, &ss, &dd, &gg, &pc, &pm};
+  return cudaLaunchCooperativeKernel((const void*)fft_conv_kernel, dim3(fold_grid(p.P)),
+                                     dim3(kFftThreads), args, smem, st);
 }
 
-// Forward transform of the packed W: rows [0, nz_rows) nonzero; result in T
-// (transposed spectrum).
-inline void fft2_forward(const FftPlan& p, int nz_rows, const int* gate, cudaStream_t st) {
-  const size_t smem = (size_t)p.P * sizeof(double2);
-  fft_rows_kernel<<<row_grid(nz_rows, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, 0,
-                                                                          nz_rows, p.tw, 0, gate);
-  dim3 tb(32, 8);
-  transpose_kernel<<<tile_grid(p.P), tb, 0, st>>>(p.W, p.T, p.P, gate);
-  fft_rows_kernel<<<row_grid(p.P, p.P), fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P,
-                                                                      p.tw, 0, gate);
+// D = deformation(u), gated; clears gate and pending count.
+inline cudaError_t fft_fold(const FftPlan& p, const double* u, double* D, int* gate,
+                            int* pending_count, cudaStream_t st) {
+  return fft_conv_launch(p, u, D, gate, pending_count, 0, st);
 }
-
-// Sets cudaFuncAttributeMaxDynamicSharedMemorySize for the row kernel.
-inline cudaError_t fft_prepare(int P) {
-  return cudaFuncSetAttribute(fft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(P * sizeof(double2)));
+inline cudaError_t fft_deformation(const FftPlan& p, const double* u, double* D, int* gate,
+                                   int* pending_count, cudaStream_t st) {
+  return fft_conv_launch(p, u, D, gate, pending_count, 0, st);
 }
 
 // Kernel spectrum KT for the table (N x N).
-inline void fft_plan_kernel(const FftPlan& p, const double* table, cudaStream_t st) {
-  const size_t PP = (size_t)p.P * p.P;
+inline cudaError_t fft_plan_kernel(const FftPlan& p, const double* table, cudaStream_t st) {
   fft_twiddles<<<(p.P / 2 + 255) / 256, 256, 0, st>>>(p.tw, p.P);
-  pack_kernel<<<ew_grid(PP), 256, 0, st>>>(p.W, p.P, p.n, table, 1, nullptr);
-  // the mirrored table has 2n+1 rows; with P = 2n the row 2n wraps onto row 0,
-  // which holds the same tap t[n] (so P = 2n is exact for the central window)
-  fft2_forward(p, 2 * p.n + 1 < p.P ? 2 * p.n + 1 : p.P, nullptr, st);
-  cudaMemcpyAsync(p.KT, p.T, PP * sizeof(double2), cudaMemcpyDeviceToDevice, st);
+  return fft_conv_launch(p, table, nullptr, nullptr, nullptr, 1, st);
 }
 
-// D = deformation(u), gated; clears gate and pending count at the end.
-inline void fft_deformation(const FftPlan& p, const double* u, double* D, int* gate,
-                            int* pending_count, cudaStream_t st) {
-  const size_t PP = (size_t)p.P * p.P;
-  const int N = p.n + 1;
-  pack_kernel<<<ew_grid(PP), 256, 0, st>>>(p.W, p.P, p.n, u, 0, gate);
-  fft2_forward(p, N, gate, st);
-  cmul_kernel<<<ew_grid(PP), 256, 0, st>>>(p.T, p.KT, PP, gate);
-  const size_t smem = (size_t)p.P * sizeof(double2);
-  fft_rows_kernel<<<row_grid(p.P, p.P), fft_threads(p.P), smem, st>>>(p.T, p.P, p.logP, 0, p.P,
-                                                                      p.tw, 1, gate);
-  dim3 tb(32, 8);
-  transpose_kernel<<<tile_grid(p.P), tb, 0, st>>>(p.T, p.W, p.P, gate);
-  // output rows n..2n; with P = 2n the last one wraps to row 0
-  const int r1 = p.n + N <= p.P ? N : p.P - p.n;
-  fft_rows_kernel<<<row_grid(r1, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, p.n, r1,
-                                                                     p.tw, 1, gate);
-  if (r1 < N)
-    fft_rows_kernel<<<row_grid(N - r1, p.P), fft_threads(p.P), smem, st>>>(p.W, p.P, p.logP, 0,
-                                                                           N - r1, p.tw, 1, gate);
-  extract_kernel<<<ew_grid((size_t)N * N), 256, 0, st>>>(p.W, p.P, p.n, D, gate, pending_count);
-  gate_clear_kernel<<<1, 32, 0, st>>>(gate, pending_count);
-}
-
+inline size_t fft_w_elems(int P) { return (size_t)P * (P / 2 + 1); }
+inline size_t fft_kt_elems(int P) { return (size_t)(P / 2 + 1) * P; }
 
 }  // namespace paqif
