@@ -196,6 +196,22 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
     out["config1"] = {"metric": "EHL Newton iters/s (line, N=513, M=20, L=10, B=1)",
                       "value": 1e3 / ms1, "unit": "iters/s", "us_per_iter": ms1 * 1e3,
                       "gpu_launches_per_iter": 1}
+    # end to end through the public solve_ehl (device-side stop tests, one
+    # host synchronisation per 32 iterations; initial state uploaded, final
+    # state read back inside the timed region)
+    from paper_2008_03276_b200.ehl import solve_ehl
+    from paper_2008_03276_b200.errors import NonConvergenceError
+    k_e2e = max(steps1, 64)
+    for rep in range(2):  # first call warms the caches
+        t0 = time.perf_counter()
+        try:
+            solve_ehl(p1, 512, tol=0.0, tol_fb=0.0, max_outer=k_e2e)
+        except NonConvergenceError:
+            pass
+        dt = time.perf_counter() - t0
+    out["config1"]["e2e"] = {"value": k_e2e / dt, "unit": "iters/s",
+                             "path": f"solve_ehl(max_outer={k_e2e}), device-side stop tests",
+                             "h2d_bytes": 513 * 8 * 2, "d2h_bytes": 513 * 8 + 48}
     cases = config3_cases(rank)
     b3 = LineContactBatch([_line_params(m, l) for m, l in cases], 1024)
     ms3 = timed(b3, steps3)

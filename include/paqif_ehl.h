@@ -56,6 +56,36 @@ int paqif_ehl_line_step(const paqif_ehl_line_cfg *cfg, int64_t B, const double *
                         double *film, double *res, double *deficit, int32_t *info,
                         uint32_t flags, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Device-side solve_ehl loop for line contacts (ehl/solver.py:210-240), one
+ * record per case.  The stop and divergence tests run in the kernel epilogue
+ * with the reference's comparisons, so a case that stopped turns every later
+ * launch into a no-op and the host only synchronises once per chunk. */
+typedef struct {
+  double tol, tol_fb;   /* stop test: res <= tol and |deficit| <= tol_fb       */
+  double best;          /* best residual so far (start +inf)                   */
+  double deficit;       /* |deficit| of the last force balance (start +inf)    */
+  int32_t max_outer;    /* iteration budget                                    */
+  int32_t outer;        /* iterations done (also the force-balance phase)      */
+  int32_t grow;         /* iterations without a new best residual              */
+  int32_t done;         /* 0 running, 1 converged, 2 diverging (grow >= 20 and
+                           res > 1e3 max(best, tol)), 3 budget spent, 4 every
+                           Ls4 rung broke down, 5 non-finite change            */
+} paqif_ehl_line_drive;
+
+/* Enqueues `steps` outer iterations of paqif_ehl_line_step for every case
+ * still running (drive[b].done == 0), taking the iteration index from
+ * drive[b].outer.  Iteration k of case b writes its residual and its load
+ * deficit (NaN when no force balance ran) to hist_res / hist_def
+ * [b * hist_cap + k % hist_cap] ([dev], may be NULL).  Other arguments as in
+ * paqif_ehl_line_step; cfg->outer is ignored. */
+int paqif_ehl_line_drive_steps(const paqif_ehl_line_cfg *cfg, int64_t B, int32_t steps,
+                               const double *table, const double *p_hertz, const double *lam,
+                               double *u, double *h0, double *film, double *res,
+                               double *deficit, int32_t *info, paqif_ehl_line_drive *drive,
+                               double *hist_res, double *hist_def, int32_t hist_cap,
+                               uint32_t flags, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
 /* Complementarity residual max|min(u, -R(u))|/h and film of B line states
  * (EhlState.complementarity_residual / film_field, ehl/solver.py:40-51);
  * [dev] pointers as in paqif_ehl_line_step, film may be NULL. */

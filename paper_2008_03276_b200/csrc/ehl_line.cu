@@ -228,16 +228,55 @@ ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restri
   if (threadIdx.x == 0) res_out[b] = cmax / c.h;
 }
 
+// solve_ehl's per-iteration bookkeeping and stop / divergence tests
+// (ehl/solver.py:219-240), same comparisons in the same order.
+__device__ void line_drive_update(paqif_ehl_line_drive& d, double res, int fb, double deficit,
+                                  int finite, double* hist_res, double* hist_def, int hist_cap,
+                                  int64_t b) {
+  const int k = d.outer;
+  if (hist_res && hist_cap > 0) {
+    hist_res[b * hist_cap + k % hist_cap] = res;
+    hist_def[b * hist_cap + k % hist_cap] = fb ? deficit : __longlong_as_double(0x7ff8000000000000ll);
+  }
+  if (fb) d.deficit = fabs(deficit);
+  d.outer = k + 1;
+  if (!finite) {  // the host driver raises after this step
+    d.done = 5;
+    return;
+  }
+  if (res <= d.tol && fabs(d.deficit) <= d.tol_fb) {
+    d.done = 1;
+    return;
+  }
+  if (res < d.best) {
+    d.best = res;
+    d.grow = 0;
+  } else {
+    d.grow += 1;
+    if (d.grow >= 20 && res > 1e3 * fmax(d.best, d.tol)) {
+      d.done = 2;
+      return;
+    }
+  }
+  if (d.outer >= d.max_outer) d.done = 3;
+}
+
 template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kEhlThreads, 1)
 ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                 const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
                 double* h0_io, double* film_out, double* res_out, double* deficit_out,
-                int32_t* info_out, char* ws, size_t ws_per_case)
+                int32_t* info_out, char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv,
+                double* hist_res, double* hist_def, int hist_cap)
 {
   extern __shared__ __align__(16) double esm[];
   const int64_t b = blockIdx.x;
   if (b >= B) return;
+  int outer = c.outer;
+  if (drv) {  // device-driven solve_ehl: stopped cases skip
+    if (drv[b].done) return;
+    outer = drv[b].outer;
+  }
   const int n = c.n, N = n + 1, n_int = n - 1;
   const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
   const EhlSmemLayout L(n);
@@ -353,6 +392,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
       res_out[b] = __longlong_as_double(0x7ff8000000000000ll);
       if (deficit_out) deficit_out[b] = __longlong_as_double(0x7ff8000000000000ll);
       info_out[b] = 1 << 8;
+      if (drv) drv[b].done = 4;
     }
     return;
   }
@@ -384,7 +424,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   __syncthreads();
   int fb = 0;
   double deficit_v = __longlong_as_double(0x7ff8000000000000ll);
-  if ((c.outer + 1) % c.force_every == 0) {
+  if ((outer + 1) % c.force_every == 0) {
     double part = 0.0;
     for (int i = threadIdx.x; i < N; i += blockDim.x) part += sun[i];
     const double total = block_sum(part, red);
@@ -406,6 +446,8 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     // info: bits 0-1 rung+1 (0 combined), bit 2 force balance applied,
     // bit 3 non-finite change, bits 16.. weighted rows
     info_out[b] = (rung + 1) | (fb << 2) | ((fin_all ? 0 : 1) << 3) | (weighted_rows << 16);
+    if (drv) line_drive_update(drv[b], cmax / h, fb, deficit_v, fin_all, hist_res, hist_def,
+                               hist_cap, b);
   }
 }
 
@@ -425,14 +467,15 @@ extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
   return (size_t)B * ((per + 255) & ~(size_t)255);
 }
 
-extern "C" int paqif_ehl_line_step(const paqif_ehl_line_cfg* cfg, int64_t B, const double* table,
-                                   const double* p_hertz, const double* lam, double* u,
-                                   double* h0, double* film, double* res, double* deficit,
-                                   int32_t* info, uint32_t flags, void* workspace,
-                                   size_t workspace_bytes, void* stream)
-{
-  if (!cfg || B < 0 || cfg->n < 4 || cfg->force_every < 1) return set_arg_error("ehl_line: bad cfg");
-  if (B == 0) return PAQIF_OK;
+namespace {
+int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const double* table,
+                const double* p_hertz, const double* lam, double* u, double* h0, double* film,
+                double* res, double* deficit, int32_t* info, paqif_ehl_line_drive* drv,
+                double* hist_res, double* hist_def, int32_t hist_cap, uint32_t flags,
+                void* workspace, size_t workspace_bytes, void* stream, const char* who) {
+  if (!cfg || B < 0 || cfg->n < 4 || cfg->force_every < 1 || steps < 0)
+    return set_arg_error("ehl_line: bad cfg");
+  if (B == 0 || steps == 0) return PAQIF_OK;
   const size_t need = paqif_ehl_line_workspace_bytes(B, cfg->n);
   if (workspace_bytes < need) return set_arg_error("ehl_line: workspace too small");
   const EhlSmemLayout L(cfg->n);
@@ -440,18 +483,42 @@ extern "C" int paqif_ehl_line_step(const paqif_ehl_line_cfg* cfg, int64_t B, con
   if (smem > 227 * 1024) return set_arg_error("ehl_line: grid too fine for one CTA");
   const size_t per = need / (size_t)B;
   cudaStream_t st = (cudaStream_t)stream;
-  if (flags & PAQIF_FLAG_EXACT) {
-    auto kern = L.sys_in_smem ? ehl_line_kernel<true, true> : ehl_line_kernel<true, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(
-        *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
-  } else {
-    auto kern = L.sys_in_smem ? ehl_line_kernel<false, true> : ehl_line_kernel<false, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(
-        *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per);
-  }
-  return check_launch("paqif_ehl_line_step");
+  auto kern = (flags & PAQIF_FLAG_EXACT)
+                  ? (L.sys_in_smem ? ehl_line_kernel<true, true> : ehl_line_kernel<true, false>)
+                  : (L.sys_in_smem ? ehl_line_kernel<false, true> : ehl_line_kernel<false, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int32_t s = 0; s < steps; ++s)
+    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(*cfg, B, table, p_hertz, lam, u, h0, film, res,
+                                                 deficit, info, (char*)workspace, per, drv,
+                                                 hist_res, hist_def, hist_cap);
+  return check_launch(who);
+}
+}  // namespace
+
+extern "C" int paqif_ehl_line_step(const paqif_ehl_line_cfg* cfg, int64_t B, const double* table,
+                                   const double* p_hertz, const double* lam, double* u,
+                                   double* h0, double* film, double* res, double* deficit,
+                                   int32_t* info, uint32_t flags, void* workspace,
+                                   size_t workspace_bytes, void* stream)
+{
+  return line_launch(cfg, B, 1, table, p_hertz, lam, u, h0, film, res, deficit, info, nullptr,
+                     nullptr, nullptr, 0, flags, workspace, workspace_bytes, stream,
+                     "paqif_ehl_line_step");
+}
+
+extern "C" int paqif_ehl_line_drive_steps(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps,
+                                          const double* table, const double* p_hertz,
+                                          const double* lam, double* u, double* h0, double* film,
+                                          double* res, double* deficit, int32_t* info,
+                                          paqif_ehl_line_drive* drive, double* hist_res,
+                                          double* hist_def, int32_t hist_cap, uint32_t flags,
+                                          void* workspace, size_t workspace_bytes, void* stream)
+{
+  if (!drive || (hist_res && !hist_def) || (hist_res && hist_cap < 1))
+    return set_arg_error("ehl_line_drive_steps: bad drive / history");
+  return line_launch(cfg, B, steps, table, p_hertz, lam, u, h0, film, res, deficit, info, drive,
+                     hist_res, hist_def, hist_cap, flags, workspace, workspace_bytes, stream,
+                     "paqif_ehl_line_drive_steps");
 }
 
 namespace paqif {

@@ -43,6 +43,10 @@ def _bind(L):
     L.paqif_ehl_line_step.argtypes = [ctypes.POINTER(LineCfg), i64, vp, vp, vp, vp, vp, vp, vp,
                                       vp, vp, u32, vp, sz, vp]
     L.paqif_ehl_line_step.restype = ctypes.c_int
+    L.paqif_ehl_line_drive_steps.argtypes = [ctypes.POINTER(LineCfg), i64, ctypes.c_int32, vp,
+                                             vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             ctypes.c_int32, u32, vp, sz, vp]
+    L.paqif_ehl_line_drive_steps.restype = ctypes.c_int
     L.paqif_ehl_line_residual.argtypes = [ctypes.POINTER(LineCfg), i64, vp, vp, vp, vp, vp, vp,
                                           vp, vp]
     L.paqif_ehl_line_residual.restype = ctypes.c_int
@@ -50,6 +54,14 @@ def _bind(L):
     L.paqif_line_deformation.restype = ctypes.c_int
     L._ehl_bound = True
     return L
+
+
+# mirror of paqif_ehl_line_drive (include/paqif_ehl.h)
+DRIVE_DTYPE = np.dtype([("tol", "<f8"), ("tol_fb", "<f8"), ("best", "<f8"), ("deficit", "<f8"),
+                        ("max_outer", "<i4"), ("outer", "<i4"), ("grow", "<i4"),
+                        ("done", "<i4")])
+DRIVE_RUNNING, DRIVE_CONVERGED, DRIVE_DIVERGING, DRIVE_BUDGET, DRIVE_BREAKDOWN, DRIVE_NONFINITE = \
+    range(6)
 
 
 def line_initial_state(params: EhlParams, intervals: int):
@@ -135,6 +147,34 @@ class LineContactBatch:
                                         _native.stream_ptr(stream))
         _native.check(rc, "paqif_ehl_line_step")
         self.outer += 1
+
+    def drive_init(self, tol: float, tol_fb: float, max_outer: int, hist_cap: int = 64):
+        """Device solve_ehl state for every case (ehl/solver.py:210-240):
+        the stop / divergence tests run on the GPU after each iteration."""
+        torch = _native.torch_cuda()
+        rec = np.zeros(self.B, dtype=DRIVE_DTYPE)
+        rec["tol"], rec["tol_fb"] = tol, tol_fb
+        rec["best"] = rec["deficit"] = np.inf
+        rec["max_outer"], rec["outer"] = max_outer, self.outer
+        self.drive = torch.from_numpy(rec.view(np.uint8)).cuda()
+        self.hist_cap = int(hist_cap)
+        self.hist_res = torch.empty((self.B, self.hist_cap), dtype=torch.float64, device="cuda")
+        self.hist_def = torch.empty_like(self.hist_res)
+
+    def drive_steps(self, steps: int, stream=None) -> None:
+        """Enqueue `steps` device-driven iterations (stopped cases skip)."""
+        rc = self.L.paqif_ehl_line_drive_steps(
+            ctypes.byref(self.cfg), self.B, int(steps), self.table.data_ptr(),
+            self.p_hertz.data_ptr(), self.lam.data_ptr(), self.u.data_ptr(), self.h0.data_ptr(),
+            self.film.data_ptr(), self.res.data_ptr(), self.deficit.data_ptr(),
+            self.info.data_ptr(), self.drive.data_ptr(), self.hist_res.data_ptr(),
+            self.hist_def.data_ptr(), self.hist_cap, self.flags, self.ws.data_ptr(),
+            self.ws_bytes, _native.stream_ptr(stream))
+        _native.check(rc, "paqif_ehl_line_drive_steps")
+
+    def drive_state(self):
+        """Host copy of the drive records (numpy structured array)."""
+        return self.drive.cpu().numpy().view(DRIVE_DTYPE).copy()
 
     def residual(self, stream=None) -> np.ndarray:
         """Complementarity residual of every case's current state (host array)."""

@@ -71,6 +71,46 @@ class _LineDriver:
     def state(self):
         return self.b.u[0].cpu().numpy(), float(self.b.h0[0].item())
 
+    def run(self, state, tol, tol_fb, max_outer, chunk=32):
+        """The whole loop on the device: chunks of `chunk` launches, one
+        synchronisation per chunk; the histories are replayed into `state`
+        exactly as the host loop appends them."""
+        from ..errors import FactorizationBreakdownError
+        from .line import (DRIVE_BREAKDOWN, DRIVE_BUDGET, DRIVE_CONVERGED, DRIVE_DIVERGING,
+                           DRIVE_NONFINITE, DRIVE_RUNNING)
+        b = self.b
+        b.drive_init(tol, tol_fb, max_outer, hist_cap=chunk)
+        done_before = 0
+        while True:
+            b.drive_steps(chunk)
+            d = b.drive_state()[0]
+            k = int(d["outer"])
+            hr = b.hist_res[0].cpu().numpy()
+            hd = b.hist_def[0].cpu().numpy()
+            last = k - 1 if d["done"] == DRIVE_NONFINITE else k  # that step raised on the host
+            for it in range(done_before, last):
+                if not np.isnan(hd[it % chunk]):
+                    state.force_history.append(abs(float(hd[it % chunk])))
+                state.residual_history.append(float(hr[it % chunk]))
+            state.outer_iterations = last
+            done_before = k
+            b.outer = k
+            if d["done"] == DRIVE_RUNNING:
+                continue
+            if d["done"] == DRIVE_CONVERGED:
+                return state
+            if d["done"] == DRIVE_BREAKDOWN:
+                raise FactorizationBreakdownError(-1, "every Ls4 rung broke down")
+            if d["done"] == DRIVE_NONFINITE:
+                raise PaqifError("non-finite change in line-contact sweep")
+            res = state.residual_history[-1]
+            if d["done"] == DRIVE_DIVERGING:
+                raise NonConvergenceError("contact iteration diverging", residual=res,
+                                          iterations=k)
+            assert d["done"] == DRIVE_BUDGET
+            raise NonConvergenceError("contact iteration exhausted its budget", residual=res,
+                                      iterations=max_outer)
+
 
 class _PointDriver:
     def __init__(self, params, intervals, state, force_every, **kw):
@@ -108,6 +148,8 @@ def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: fl
     grow = 0
     best = np.inf
     try:
+        if isinstance(drv, _LineDriver) and collect is None and max_outer > 0:
+            return drv.run(state, tol, tol_fb, max_outer)
         for outer in range(max_outer):
             res, fb = drv.step()
             if fb is not None:

@@ -141,3 +141,62 @@ def test_line_complementarity_residual(key):
     st.h0 = float(d["h0_out"])
     assert math.isclose(st.complementarity_residual(p, 1.0 / 3.0, "kappa"), float(d["res_out"]),
                         rel_tol=TOL)
+
+
+def _line_params():
+    from paper_2008_03276_b200.ehl import EhlParams, moes_convert
+    u_, w_ = moes_convert(m=20.0, l=10.0, g=5000.0)
+    return EhlParams.line_from_loads(5000.0, u_, w_, domain=(-4.5, 1.5))
+
+
+@pytest.mark.parametrize("tol,tol_fb,max_outer", [(1e-6, 1e-4, 70), (1e30, 1e30, 40),
+                                                  (1e30, 1e-300, 12)])
+def test_device_driver_matches_host_loop(tol, tol_fb, max_outer):
+    """solve_ehl without `collect` runs the stop / divergence tests on the
+    device (paqif_ehl_line_drive_steps, chunks of 32 launches); with
+    `collect` it steps from the host.  Same histories, state and outcome."""
+    from paper_2008_03276_b200.ehl import solve_ehl
+    from paper_2008_03276_b200.errors import NonConvergenceError
+    p = _line_params()
+    out = []
+    for collect in (None, lambda st, r, d: None):
+        err = None
+        try:
+            st = solve_ehl(p, 512, tol=tol, tol_fb=tol_fb, max_outer=max_outer, collect=collect)
+        except NonConvergenceError as e:
+            err, st = (e.iterations, e.residual), None
+        out.append((err, st))
+    (e_dev, s_dev), (e_host, s_host) = out
+    assert e_dev == e_host
+    if s_dev is not None:
+        assert s_dev.residual_history == s_host.residual_history
+        assert s_dev.force_history == s_host.force_history
+        assert s_dev.outer_iterations == s_host.outer_iterations
+        assert np.array_equal(s_dev.u, s_host.u) and s_dev.h0 == s_host.h0
+
+
+def test_device_driver_batch_stops_per_case():
+    """Per-case drive records: a case that converged skips later launches
+    while the others keep iterating."""
+    import torch
+    from paper_2008_03276_b200.ehl.line import DRIVE_BUDGET, DRIVE_CONVERGED, LineContactBatch
+    p = _line_params()
+    b = LineContactBatch([p, p], 512)
+    b.drive_init(1e30, 1e30, 9, hist_cap=16)
+    rec = b.drive_state()
+    rec["tol_fb"][1] = 1e-300  # case 1 can never pass the force test
+    b.drive.copy_(torch.from_numpy(rec.view(np.uint8)))
+    b.drive_steps(16)
+    d = b.drive_state()
+    assert d["done"][0] == DRIVE_CONVERGED and d["outer"][0] == 5
+    assert d["done"][1] == DRIVE_BUDGET and d["outer"][1] == 9
+    ref = LineContactBatch([p], 512)
+    res = []
+    for k in range(9):
+        ref.step()
+        res.append(float(ref.res[0].item()))
+        if k == 4:
+            assert np.array_equal(b.u[0].cpu().numpy(), ref.u[0].cpu().numpy())
+    assert np.array_equal(b.u[1].cpu().numpy(), ref.u[0].cpu().numpy())
+    assert list(b.hist_res[0, :5].cpu().numpy()) == res[:5]
+    assert list(b.hist_res[1, :9].cpu().numpy()) == res
