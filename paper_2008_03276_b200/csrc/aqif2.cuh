@@ -147,10 +147,9 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
       oc[e] = rk[oth_crs + e];
     }
     const double ym = rk[12 + side], yo = rk[13 - side];
-    const double a11 = side ? oc[0] : po[0];
-    const double a12 = side ? oo[0] : pc[0];
-    const double a21 = side ? pc[0] : oo[0];
-    const double a22 = side ? po[0] : oc[0];
+    // the pivot block sits at fixed record slots for both sides (uniform
+    // loads instead of side selects)
+    const double a11 = rk[0], a12 = rk[3], a21 = rk[6], a22 = rk[9];
     const double det = A::det2(a11, a22, a21, a12);
     const double y = __drcp_rn(det);  // fast mode multiplies by it
     if (lane_id == 0) {
@@ -259,6 +258,7 @@ __device__ bool aqif2_zsolve(double* rec_, int n, int lane_id) {
   };
   if (s >= 1) level(0, 0);
   if (s >= 2) level(1, 1);
+#pragma unroll 2
   for (int p = 2; p < s; ++p) level(p, 2);
   return EXACT && !CHECKED ? __all_sync(0xffffffffu, safe) : true;
 }

@@ -10,7 +10,8 @@ __device__ uint64_t mix(uint64_t x) {
   x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
   return x;
 }
-__global__ void k(unsigned long long* bad, unsigned long long* unsafe_cnt, int mode, int iters) {
+__global__ void k(unsigned long long* bad, unsigned long long* unsafe_cnt, int mode, int iters,
+                  unsigned long long* bad_fix) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (int it = 0; it < iters; ++it) {
     uint64_t h = mix(tid * 1000003ull + it * 7919ull + mode * 0x9e3779b97f4a7c15ull);
@@ -31,6 +32,12 @@ __global__ void k(unsigned long long* bad, unsigned long long* unsafe_cnt, int m
     bool safe = true;
     const double q1 = mdiv(a, b, y, safe);
     const double q2 = __ddiv_rn(a, b);
+    bool safe_fix = true;
+    const double q3 = mdiv_fix(a, b, y, safe_fix);
+    if (safe_fix && __double_as_longlong(q3) != __double_as_longlong(q2)) {
+      const unsigned long long c = atomicAdd(bad_fix, 1ull);
+      if (c < 6) printf("a=%a b=%a mdiv_fix=%a ieee=%a\n", a, b, q3, q2);
+    }
     if (!safe) {
       const unsigned long long c = atomicAdd(unsafe_cnt, 1ull);
       if (c < 3) printf("unsafe: a=%a b=%a\n", a, b);
@@ -42,12 +49,13 @@ __global__ void k(unsigned long long* bad, unsigned long long* unsafe_cnt, int m
   }
 }
 int main() {
-  unsigned long long *d, h[2];
-  cudaMalloc(&d, 16);
+  unsigned long long *d, h[3];
+  cudaMalloc(&d, 24);
   for (int mode = 0; mode < 2; ++mode) {
-    cudaMemset(d, 0, 16);
-    k<<<1184, 256>>>(d, d + 1, mode, 64);
-    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("mode %d: %d samples, mismatches %llu, flagged unsafe %llu\n", mode, 1184 * 256 * 64, h[0], h[1]);
+    cudaMemset(d, 0, 24);
+    k<<<1184, 256>>>(d, d + 1, mode, 64, d + 2);
+    cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+    printf("mode %d: %d samples, mdiv mismatches %llu, flagged unsafe %llu; mdiv_fix mismatches %llu\n",
+           mode, 1184 * 256 * 64, h[0], h[1], h[2]);
   }
 }
