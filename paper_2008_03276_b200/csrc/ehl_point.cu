@@ -62,7 +62,14 @@ struct PointDev {
   int32_t* yinfo;   // n-1: rung
   double* film_out; // N x N
   double* rcache;   // 8 x N: rheology (eps, rho) of the points a line reads
+  // batched runs of deferred x-lines (see enqueue_x_sweep)
+  double* run_films;  // N x N: films of rows a-1 .. b of a run [a, b)
+  double* run_rc;     // 2 x N x N: their eps (first N x N) and rho
+  int32_t* run_flag;  // N: line a+l is deferred (by its own decision)
+  int32_t* done;      // N: line j was solved inside a batched run
+  double* run_scratch;  // kRunCtas line systems when they do not fit in shared memory
 };
+constexpr int kRunCtas = 148;
 
 __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_ehl_point_cfg& c,
                                            double& rho) {
@@ -91,7 +98,12 @@ __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_eh
 constexpr int kPtFilmWarps = 8;
 __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
                                                                      paqif_ehl_point_cfg c,
-                                                                     int mode, int first, int L) {
+                                                                     int mode, int first, int L,
+                                                                     double* films_out,
+                                                                     double* rc_out,
+                                                                     size_t rho_off,
+                                                                     const int32_t* skip) {
+  if (skip && *skip) return;  // the line was solved in a batched run
   const int N = d.N;
   const int count = d.meta[kMCount];
   const double h0 = d.scal[0];
@@ -105,10 +117,10 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
   // film value o plus its rheology (eps, rho) for the line kernel: the
   // pointwise work of a line spread over the whole GPU
   auto emit = [&](int o, int line, int idx, double v) {
-    d.films[o] = v;
+    films_out[o] = v;
     double rho;
-    d.rcache[o] = rheo_eps(d.u[gidx(line, idx)], v, c, rho);
-    d.rcache[4 * (size_t)N + o] = rho;
+    rc_out[o] = rheo_eps(d.u[gidx(line, idx)], v, c, rho);
+    rc_out[rho_off + o] = rho;
   };
   if (count == 0) {
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -247,18 +259,23 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
 
 // x-line j of _hybrid_x_sweep (solver.py:91-114) with _line_quantities
 // (sweeps.py:318-341) and assemble_line_system's point terms (sweeps.py:157-267)
+// where an x-line reads its films and rheology: rows j-1, j, j+1 at
+// films[0..3N), eps at rc[0..3N), rho at rc[rho_off ..)
+struct XSrc {
+  const double* films;
+  const double* rc;
+  size_t rho_off;
+};
+
+// One x-line of the point contact (see pt_xline_kernel); all threads of
+// the CTA call.  sysb: the line system's storage.
 template <bool EXACT, bool SMEM>
-__global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
-                                                              SweepCtl ctl, int j) {
-  extern __shared__ __align__(16) double xsm[];
-  PtShared& S = *reinterpret_cast<PtShared*>(xsm);
-  // SMEM: the line system in shared memory (address space known to the
-  // compiler -> LDS/STS in the solver's level loops)
-  double* sysb = SMEM ? xsm + sizeof(PtShared) / 8 : d.scratch;
+__device__ void xline_body(PointDev& d, const paqif_ehl_point_cfg& c, const SweepCtl& ctl, int j,
+                           const XSrc src, double* sysb, PtShared& S) {
   const int n = d.n, N = d.N, n_int = n - 1, n_sys = d.n_sys;
   const double h = c.h;
   const double* u = d.u;
-  const double* F = d.films;  // rows j-1, j, j+1
+  const double* F = src.films;  // rows j-1, j, j+1
   long long tp0 = clock64(), tp1 = 0, tp2 = 0, tp3 = 0;
   auto film = [&](int r, int i) { return F[(size_t)(r - (j - 1)) * N + i]; };
   auto eps_at = [&](int r, int i, double& rho) {
@@ -266,10 +283,10 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
   };
   // pass 1: the rheology of rows j-1, j, j+1 came with the films
   // (pt_films_kernel); min(eps_line)/h and max|q_line|
-  const double* E0 = d.rcache;
+  const double* E0 = src.rc;
   const double* E1 = E0 + N;
   const double* E2 = E1 + N;
-  const double* R1 = d.rcache + 4 * (size_t)N + N;
+  const double* R1 = src.rc + src.rho_off + N;
   double emin = INFINITY, qmax = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     emin = fmin(emin, E1[i]);
@@ -386,6 +403,60 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
     }
     if (deferred) d.meta[kMAnyW] = 1;
     if (d.prof) atomicAdd(&d.prof[3], (unsigned long long)(clock64() - tp3));
+  }
+}
+
+template <bool EXACT, bool SMEM>
+__global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
+                                                              SweepCtl ctl, int j) {
+  if (d.done[j]) return;  // solved inside a batched run of deferred lines
+  extern __shared__ __align__(16) double xsm[];
+  PtShared& S = *reinterpret_cast<PtShared*>(xsm);
+  // SMEM: the line system in shared memory (address space known to the
+  // compiler -> LDS/STS in the solver's level loops)
+  double* sysb = SMEM ? xsm + sizeof(PtShared) / 8 : d.scratch;
+  xline_body<EXACT, SMEM>(d, c, ctl, j, XSrc{d.films, d.rcache, 4 * (size_t)d.N}, sysb, S);
+}
+
+// Deferred decision of every line of a candidate run [a, a+L): the same
+// min(eps)/h test as the line kernel's pass 1, on the run's rheology rows
+// (one block per line).
+__global__ void pt_run_flags_kernel(PointDev d, paqif_ehl_point_cfg c, SweepCtl ctl, int L) {
+  __shared__ double red[32];
+  const int l = blockIdx.x;
+  if (l >= L) return;
+  const int N = d.N;
+  const double* E = d.run_rc + (size_t)(l + 1) * N;
+  double emin = INFINITY;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) emin = fmin(emin, E[i]);
+  const double ratio = block_min(emin, red) / c.h;
+  const bool weighted = ctl.sel < 0 ? !(ratio > kSwitch) : ctl.sel == 1;
+  const bool deferred = ctl.defer < 0 ? weighted : ctl.defer == 1;
+  if (threadIdx.x == 0) d.run_flag[l] = deferred ? 1 : 0;
+}
+
+// A run of deferred x-lines [a, a+L) solved side by side: deferred lines
+// leave u, the pending list and the films untouched, so in the reference's
+// Gauss-Seidel order each of them sees the same state as the run's first
+// line -- identical results, any order.  CTA-strided lines; line a+l is
+// solved only if lines a..a+l are all deferred (run_flag), else it is left
+// to the per-line launches that follow (done[] stays 0).
+template <bool EXACT, bool SMEM>
+__global__ void __launch_bounds__(kPtThreads, 1) pt_xrun_kernel(PointDev d, paqif_ehl_point_cfg c,
+                                                             SweepCtl ctl, int a, int L) {
+  extern __shared__ __align__(16) double xsm[];
+  PtShared& S = *reinterpret_cast<PtShared*>(xsm);
+  double* sysb = SMEM ? xsm + sizeof(PtShared) / 8
+                      : d.run_scratch + (size_t)blockIdx.x * pt_sys_doubles(d.n_sys);
+  const int N = d.N;
+  for (int l = blockIdx.x; l < L; l += gridDim.x) {
+    int ok = 1;
+    for (int q = threadIdx.x; q <= l; q += blockDim.x) ok &= d.run_flag[q];
+    if (!__syncthreads_and(ok)) return;  // later lines of this CTA fail the prefix too
+    const XSrc src{d.run_films + (size_t)l * N, d.run_rc + (size_t)l * N, (size_t)N * N};
+    xline_body<EXACT, SMEM>(d, c, ctl, a + l, src, sysb, S);
+    __syncthreads();
+    if (threadIdx.x == 0) d.done[a + l] = 1;
   }
 }
 
@@ -645,6 +716,12 @@ struct paqif_ehl_point {
   cudaStream_t st;
   std::vector<void*> allocs;
   size_t line_smem;
+  // previous x-sweep's per-line tags (pinned), for predicting the runs of
+  // deferred lines of the next one; valid once `xinfo_ev` completed
+  int32_t* xinfo_prev = nullptr;
+  cudaEvent_t xinfo_ev = nullptr;
+  bool xinfo_valid = false;
+  bool runs = true;  // PAQIF_PT_RUNS=0 solves every x-line on its own (A/B checks)
 };
 
 namespace {
@@ -718,6 +795,12 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.yinfo = dalloc<int32_t>(h, N);
   d.film_out = dalloc<double>(h, NN);
   d.rcache = dalloc<double>(h, 8 * (size_t)N);
+  d.run_films = dalloc<double>(h, NN);
+  d.run_rc = dalloc<double>(h, 2 * NN);
+  d.run_flag = dalloc<int32_t>(h, N);
+  d.done = dalloc<int32_t>(h, N);
+  d.run_scratch = dalloc<double>(h, d.sys_in_smem ? 32 : (size_t)kRunCtas * pt_sys_doubles(n_sys));
+  if (const char* e = getenv("PAQIF_PT_RUNS")) h->runs = e[0] != '0';
   d.prof = nullptr;
   if (const char* e = getenv("PAQIF_PT_PROF"))
     if (e[0] == '1') d.prof = dalloc<unsigned long long>(h, 8);
@@ -727,7 +810,9 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != (d.prof ? 15u : 14u)) {
+  if (h->allocs.size() != (d.prof ? 20u : 19u) ||
+      cudaMallocHost((void**)&h->xinfo_prev, (size_t)N * sizeof(int32_t)) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->xinfo_ev, cudaEventDisableTiming) != cudaSuccess) {
     paqif_ehl_point_destroy(h);
     set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
     return nullptr;
@@ -764,6 +849,8 @@ extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
   }
   for (void* a : h->allocs)
     if (a) cudaFree(a);
+  if (h->xinfo_prev) cudaFreeHost(h->xinfo_prev);
+  if (h->xinfo_ev) cudaEventDestroy(h->xinfo_ev);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -796,11 +883,43 @@ void prepare_attrs(paqif_ehl_point* h) {
   cudaFuncSetAttribute(pt_xline_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pt_yline_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(pt_yline_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_xrun_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(pt_xrun_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   done = true;
 }
 
+// Runs [a, b) of deferred lines for this x-sweep: every line when all
+// updates are deferred (weighted_change_sweep); for the hybrid sweep the
+// previous x-sweep's deferred runs (the weighted block in the contact is
+// stable from one outer iteration to the next) -- a prediction only: the
+// run kernel checks every line's own decision and leaves the rest to the
+// per-line launches.
+std::vector<std::pair<int, int>> x_runs(paqif_ehl_point* h, const SweepCtl& ctl) {
+  std::vector<std::pair<int, int>> runs;
+  const int n = h->d.n;
+  if (!h->runs) return runs;
+  if (ctl.defer == 1) {
+    runs.emplace_back(1, n);
+  } else if (ctl.defer < 0 && ctl.sel != 0 && h->xinfo_valid &&
+             cudaEventQuery(h->xinfo_ev) == cudaSuccess) {
+    constexpr int kMinRun = 4;
+    int a = -1;
+    for (int j = 1; j <= n; ++j) {
+      const bool dfr = j < n && (h->xinfo_prev[j - 1] & 2) != 0;
+      if (dfr && a < 0) a = j;
+      if (!dfr && a >= 0) {
+        if (j - a >= kMinRun) runs.emplace_back(a, j);
+        a = -1;
+      }
+    }
+  }
+  return runs;
+}
+
 // x-direction sweep: lines j = 1..n-1 in order, each followed by the gated
-// fold; deferred changes applied (and folded) at the end.
+// fold; deferred changes applied (and folded) at the end.  Runs of deferred
+// lines are solved side by side first (pt_xrun_kernel); the per-line
+// launches of a line the run solved return at once (done[j]).
 void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   PointDev& d = h->d;
   const int n = d.n, N = d.N;
@@ -808,8 +927,33 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   const size_t NN = (size_t)N * N;
   cudaMemsetAsync(d.sigma, 0, NN * 8, st);
   cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
+  cudaMemsetAsync(d.done, 0, (size_t)N * sizeof(int32_t), st);
+  const auto runs = x_runs(h, ctl);
+  size_t next_run = 0;
+  const bool certain = ctl.defer == 1;  // every line deferred: no per-line launches needed
   for (int j = 1; j < n; ++j) {
-    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(d, h->cfg, 0, j - 1, 3);
+    if (next_run < runs.size() && runs[next_run].first == j) {
+      const int a = runs[next_run].first, L = runs[next_run].second - a;
+      ++next_run;
+      // films + rheology of rows a-1 .. a+L, the deferred flags, the run
+      pt_films_kernel<<<film_blocks(N, L + 2), 32 * kPtFilmWarps, 0, st>>>(
+          d, h->cfg, 0, a - 1, L + 2, d.run_films, d.run_rc, NN, nullptr);
+      pt_run_flags_kernel<<<L, 256, 0, st>>>(d, h->cfg, ctl, L);
+      const unsigned g = (unsigned)(L < kRunCtas ? L : kRunCtas);
+      if (d.sys_in_smem) {
+        if (exact) pt_xrun_kernel<true, true><<<g, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, a, L);
+        else pt_xrun_kernel<false, true><<<g, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, a, L);
+      } else {
+        if (exact) pt_xrun_kernel<true, false><<<g, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, a, L);
+        else pt_xrun_kernel<false, false><<<g, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, a, L);
+      }
+      if (certain) {
+        j = a + L - 1;
+        continue;
+      }
+    }
+    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(
+        d, h->cfg, 0, j - 1, 3, d.films, d.rcache, 4 * (size_t)N, &d.done[j]);
     if (d.sys_in_smem) {
       if (exact) pt_xline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
       else pt_xline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
@@ -825,6 +969,13 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
     pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 1);
     fold(h);
   }
+  // this sweep's tags: the next hybrid sweep's run prediction
+  if (ctl.defer < 0 && ctl.sel < 0) {
+    cudaMemcpyAsync(h->xinfo_prev, d.xinfo, (size_t)(n - 1) * sizeof(int32_t),
+                    cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(h->xinfo_ev, st);
+    h->xinfo_valid = true;
+  }
 }
 
 void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
@@ -834,7 +985,8 @@ void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   for (int i = 1; i < n; ++i) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
-    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(d, h->cfg, 1, lo, L);
+    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(
+        d, h->cfg, 1, lo, L, d.films, d.rcache, 4 * (size_t)N, nullptr);
     if (d.sys_in_smem) {
       if (exact) pt_yline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
       else pt_yline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);

@@ -155,3 +155,28 @@ def test_public_sweeps_vs_reference(name):
     assert close_field(st.u, ref)
     assert np.array_equal(st.u == 0.0, ref == 0.0)
     assert math.isclose(val, float(d["value"]), rel_tol=TOL)
+
+
+@pytest.mark.parametrize("n,steps", [(64, 4), (128, 3)])
+def test_batched_deferred_runs_match_line_by_line(monkeypatch, n, steps):
+    """Runs of deferred x-lines solved side by side (pt_xrun_kernel, runs
+    predicted from the previous sweep) give bit-identical states, tags and
+    residuals to solving every line on its own in Gauss-Seidel order."""
+    from paper_2008_03276_b200.ehl import PointContact
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PAQIF_PT_RUNS", flag)
+        pc = PointContact(params_for(100.0), n)
+        hist = []
+        for _ in range(steps):
+            pc.step()
+            hist.append(pc.status()[1])
+        s = pc.snapshot()
+        pc.close()
+        out.append((hist, s))
+    (h1, s1), (h0, s0) = out
+    assert h1 == h0
+    assert np.array_equal(s1["u"], s0["u"]) and s1["h0"] == s0["h0"]
+    assert np.array_equal(s1["newton"], s0["newton"])
+    assert np.array_equal(s1["x_rungs"], s0["x_rungs"])
+    assert int(np.sum(np.asarray(s1["newton"]) == 0)) >= 4, "no deferred run to batch"
