@@ -18,6 +18,7 @@
 #include <vector>
 #include "ehl_common.cuh"
 #include "aqif2.cuh"
+#include "aqif1.cuh"
 #include "fft_deform.cuh"
 #include "capi_util.cuh"
 
@@ -253,6 +254,19 @@ __device__ __forceinline__ void put_row(double* band, double* rhs, int n_sys, in
     const int col = r + dd - kLineBeta;
     const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (dd == kLineBeta);
     band2_ref(band, n_sys, r, dd - kLineBeta) = keep ? e[dd] : 0.0;
+  }
+  rhs[kBandPad + r] = rr;
+}
+
+// the same for the tridiagonal column systems (aqif1 layout, offsets -1..1
+// from e[1..3])
+__device__ __forceinline__ void put_row1(double* band, double* rhs, int n_sys, int n_int, int r,
+                                         const double* e, double rr) {
+#pragma unroll
+  for (int dd = 1; dd < 4; ++dd) {
+    const int col = r + dd - kLineBeta;
+    const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (dd == kLineBeta);
+    band1_ref(band, n_sys, r, dd - kLineBeta) = keep ? e[dd] : 0.0;
   }
   rhs[kBandPad + r] = rr;
 }
@@ -520,9 +534,10 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
   const double* t = d.table;
   const double s00 = t[0], s10 = t[N], s01 = t[1], s11 = t[N + 1];
   double* band = sysb;
-  double* rhs = band + aqif2_band_doubles(n_sys);
-  double* rec = rhs + aqif2_rhs_doubles(n_sys);
-  aqif2_zero_pads(band, rhs, n_sys);
+  // tridiagonal: the reference factors these with beta = 1 (aqif1.cuh)
+  double* rhs = band + aqif1_band_doubles(n_sys);
+  double* rec = rhs + aqif1_rhs_doubles(n_sys);
+  aqif1_zero_pads(band, rhs, n_sys);
   int st = 1, rung = 0;
   double worst = 0.0;
   for (; rung < 2; ++rung) {  // 0: tridiagonal system, 1: diagonal fallback
@@ -575,10 +590,10 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
           e[2] = (ey_p + ey_m + ex_p + ex_m) / h + h * fabs(rc) * s00;
         }
       }
-      put_row(band, rhs, n_sys, n_int, r, e, rr);
+      put_row1(band, rhs, n_sys, n_int, r, e, rr);
     }
     if (rung == 0) note_worst(d, worst, S.red);
-    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, band, &S.flag) & 1;
+    st = aqif1_solve<EXACT>(band, rhs, n_sys, rec, band, &S.flag) & 1;
     if (!st) break;
   }
   if (st) {
@@ -588,7 +603,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
     }
     return;
   }
-  const double* x = band;  // aqif2_solve wrote x over the band
+  const double* x = band;  // aqif1_solve wrote x over the band
   int nz = 0, fin = 1;
   double* delta = d.pend + (size_t)d.meta[kMCount] * N;
   for (int m = threadIdx.x; m < N; m += blockDim.x) {
