@@ -69,6 +69,7 @@ struct PointDev {
   int32_t* run_flag;  // N: line a+l is deferred (by its own decision)
   int32_t* done;      // N: line j was solved inside a batched run
   double* run_scratch;  // kRunCtas line systems when they do not fit in shared memory
+  double* fpart;        // films: per-k-segment partial corrections (kFilmSegMax x 4 x N)
 };
 constexpr int kRunCtas = 148;
 
@@ -89,6 +90,72 @@ __device__ __forceinline__ double rheo_eps(double u, double film, const paqif_eh
   return coeff * (gap * gap * gap);
 }
 
+// Pending-line corrections of the films of L <= 4 lines when every pending
+// update lies along the sweep axis (the common case): per pending p and
+// output line l a Toeplitz product  sum_k t_{|line - ell_p|}[|idx - k|]
+// delta_p[k].  One warp per (128 outputs, k segment of 128, p):
+// register-tiled, 4 consecutive outputs per lane, one shared load of the
+// kernel window and one broadcast delta per 4 FMAs, so a single line's
+// films fill the GPU.  Writes part[((p * nseg + seg) * 4 + l) * N + idx];
+// pt_films_kernel sums the parts in a fixed order.  Does nothing when any
+// pending update is cross-axis (pt_films_kernel then does it all).
+constexpr int kFilmKS = 128;     // k per segment
+constexpr int kFilmChunk = 128;  // outputs per warp: 32 lanes x 4
+constexpr int kFilmSegMax = 32;  // N <= 4096
+__global__ void __launch_bounds__(32) pt_films_part_kernel(PointDev d, int mode, int first, int L,
+                                                           const int32_t* skip) {
+  if (skip && *skip) return;
+  const int count = d.meta[kMCount];
+  const int p = blockIdx.z;
+  if (p >= count) return;
+  for (int q = 0; q < count; ++q)
+    if (d.meta[kMAxis + q] != mode) return;
+  const int N = d.N;
+  const int nch = (N + kFilmChunk - 1) / kFilmChunk, nseg = gridDim.y;
+  const int l = blockIdx.x / nch, ch = blockIdx.x % nch, seg = blockIdx.y;
+  if (l >= L) return;
+  const int line = first + l;
+  const int idx0 = ch * kFilmChunk, k0 = seg * kFilmKS;
+  const int k1 = k0 + kFilmKS < N ? k0 + kFilmKS : N;
+  const int nk = k1 - k0;
+  __shared__ double sd[kFilmKS];
+  __shared__ double se[kFilmChunk + kFilmKS + 4];  // se[1 + q] = t[|mlo + q|], se[0] = 0
+  const int mlo = idx0 - (k1 - 1);
+  const int nw = kFilmChunk + nk - 1;
+  const double* __restrict__ delta = d.pend + (size_t)p * N;
+  const double* __restrict__ tr = d.table + (size_t)abs(line - d.meta[kMIdx + p]) * N;
+  const int lane = threadIdx.x;
+  if (lane == 0) se[0] = 0.0;
+  for (int q = lane; q < nk; q += 32) sd[q] = delta[k0 + q];
+  for (int q = lane; q < nw; q += 32) {
+    const int m = abs(mlo + q);
+    se[1 + q] = m < N ? tr[m] : 0.0;
+  }
+  __syncwarp();
+  // output idx0 + 4 lane + i at k0 + kk reads se[4 lane + i + nk - kk]
+  int e = 4 * lane + nk;
+  double w0 = se[e], w1 = se[e + 1], w2 = se[e + 2], w3 = se[e + 3];
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  for (int k = 0; k < nk; ++k) {
+    const double dk = sd[k];
+    acc0 = fma(w0, dk, acc0);
+    acc1 = fma(w1, dk, acc1);
+    acc2 = fma(w2, dk, acc2);
+    acc3 = fma(w3, dk, acc3);
+    --e;
+    w3 = w2;
+    w2 = w1;
+    w1 = w0;
+    w0 = se[e];
+  }
+  double* out = d.fpart + ((size_t)(p * nseg + seg) * 4 + l) * N;
+  const int i0 = idx0 + 4 * lane;
+  if (i0 < N) out[i0] = acc0;
+  if (i0 + 1 < N) out[i0 + 1] = acc1;
+  if (i0 + 2 < N) out[i0 + 2] = acc2;
+  if (i0 + 3 < N) out[i0 + 3] = acc3;
+}
+
 // films of `L` consecutive rows (mode 0) or columns (mode 1) starting at
 // `first` (FilmModel.film_rows / film_cols, film.py:98-146).  With pending
 // line updates every output is a length-N dot product per update: one warp
@@ -103,7 +170,8 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
                                                                      double* films_out,
                                                                      double* rc_out,
                                                                      size_t rho_off,
-                                                                     const int32_t* skip) {
+                                                                     const int32_t* skip,
+                                                                     int nseg) {
   if (skip && *skip) return;  // the line was solved in a batched run
   const int N = d.N;
   const int count = d.meta[kMCount];
@@ -134,6 +202,16 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
   const int l = o / N, idx = o % N;
   const int line = first + l;
   double corr = 0.0;
+  bool cross = false;
+  for (int p = 0; p < count; ++p) cross |= d.meta[kMAxis + p] != mode;
+  if (nseg > 0 && !cross) {  // parts of pt_films_part_kernel, fixed-order sum
+    double v = 0.0;
+    for (int q = lane; q < count * nseg; q += 32) v += d.fpart[((size_t)q * 4 + l) * N + idx];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) emit(o, line, idx, base(line, idx) + v);
+    return;
+  }
   for (int p = 0; p < count; ++p) {
     const int axis = d.meta[kMAxis + p], ell = d.meta[kMIdx + p];
     const double* __restrict__ delta = d.pend + (size_t)p * N;
@@ -815,6 +893,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.run_flag = dalloc<int32_t>(h, N);
   d.done = dalloc<int32_t>(h, N);
   d.run_scratch = dalloc<double>(h, d.sys_in_smem ? 32 : (size_t)kRunCtas * pt_sys_doubles(n_sys));
+  d.fpart = dalloc<double>(h, (size_t)kMaxPending * kFilmSegMax * 4 * N);
   if (const char* e = getenv("PAQIF_PT_RUNS")) h->runs = e[0] != '0';
   d.prof = nullptr;
   if (const char* e = getenv("PAQIF_PT_PROF"))
@@ -825,7 +904,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != (d.prof ? 20u : 19u) ||
+  if (h->allocs.size() != (d.prof ? 21u : 20u) ||
       cudaMallocHost((void**)&h->xinfo_prev, (size_t)N * sizeof(int32_t)) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->xinfo_ev, cudaEventDisableTiming) != cudaSuccess) {
     paqif_ehl_point_destroy(h);
@@ -887,6 +966,28 @@ namespace {
 
 unsigned film_blocks(int N, int L) {
   return (unsigned)((L * N + kPtFilmWarps - 1) / kPtFilmWarps);
+}
+
+// films + rheology of L consecutive lines into (films_out, rc_out, rho at
+// rc_out + rho_off): tiled partial corrections and the per-output sum, four
+// lines at a time (the same arithmetic for every line, whatever L)
+void films(paqif_ehl_point* h, int mode, int first, int L, const int32_t* skip,
+           double* films_out, double* rc_out, size_t rho_off) {
+  PointDev& d = h->d;
+  const int N = d.N;
+  const int nseg = (N + kFilmKS - 1) / kFilmKS;
+  const bool tiled = nseg <= kFilmSegMax;
+  for (int l0 = 0; l0 < L; l0 += 4) {
+    const int Lc = L - l0 < 4 ? L - l0 : 4;
+    if (tiled) {
+      const dim3 grid((unsigned)(((N + kFilmChunk - 1) / kFilmChunk) * Lc), (unsigned)nseg,
+                      (unsigned)kMaxPending);
+      pt_films_part_kernel<<<grid, 32, 0, h->st>>>(d, mode, first + l0, Lc, skip);
+    }
+    pt_films_kernel<<<film_blocks(N, Lc), 32 * kPtFilmWarps, 0, h->st>>>(
+        d, h->cfg, mode, first + l0, Lc, films_out + (size_t)l0 * N, rc_out + (size_t)l0 * N,
+        rho_off, skip, tiled ? nseg : 0);
+  }
 }
 
 void prepare_attrs(paqif_ehl_point* h) {
@@ -951,8 +1052,7 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
       const int a = runs[next_run].first, L = runs[next_run].second - a;
       ++next_run;
       // films + rheology of rows a-1 .. a+L, the deferred flags, the run
-      pt_films_kernel<<<film_blocks(N, L + 2), 32 * kPtFilmWarps, 0, st>>>(
-          d, h->cfg, 0, a - 1, L + 2, d.run_films, d.run_rc, NN, nullptr);
+      films(h, 0, a - 1, L + 2, nullptr, d.run_films, d.run_rc, NN);
       pt_run_flags_kernel<<<L, 256, 0, st>>>(d, h->cfg, ctl, L);
       const unsigned g = (unsigned)(L < kRunCtas ? L : kRunCtas);
       if (d.sys_in_smem) {
@@ -967,8 +1067,7 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
         continue;
       }
     }
-    pt_films_kernel<<<film_blocks(N, 3), 32 * kPtFilmWarps, 0, st>>>(
-        d, h->cfg, 0, j - 1, 3, d.films, d.rcache, 4 * (size_t)N, &d.done[j]);
+    films(h, 0, j - 1, 3, &d.done[j], d.films, d.rcache, 4 * (size_t)N);
     if (d.sys_in_smem) {
       if (exact) pt_xline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
       else pt_xline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, j);
@@ -1000,8 +1099,7 @@ void enqueue_y_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   for (int i = 1; i < n; ++i) {
     const int lo = i - 2 > 0 ? i - 2 : 0;
     const int L = i + 2 - lo;
-    pt_films_kernel<<<film_blocks(N, L), 32 * kPtFilmWarps, 0, st>>>(
-        d, h->cfg, 1, lo, L, d.films, d.rcache, 4 * (size_t)N, nullptr);
+    films(h, 1, lo, L, nullptr, d.films, d.rcache, 4 * (size_t)N);
     if (d.sys_in_smem) {
       if (exact) pt_yline_kernel<true, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
       else pt_yline_kernel<false, true><<<1, kPtThreads, h->line_smem, st>>>(d, h->cfg, ctl, i);
