@@ -45,7 +45,7 @@ struct EhlSmemLayout {
   __host__ __device__ explicit EhlSmemLayout(int n) {
     const int N = n + 1, NA = (N + 3 + 1) & ~1;  // padded for the 4-wide conv tail
     int o = 0;
-    ext = o + 8; o += 2 * n + 1 + 16; o = (o + 1) & ~1;  // 8-element guards both ends
+    ext = o; o += ext4_doubles(n); o = (o + 1) & ~1;  // line kernel, ext4 layout
     su = o; o += NA;
     sun = o; o += NA;
     film = o; o += NA;
@@ -216,8 +216,7 @@ ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restri
   double* su = esm + L.su;
   double* sdef = esm + L.def;
   for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_in[b * N + k];
-  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
-    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  ext4_build(table, n, ext);
   __syncthreads();
   toeplitz_conv(su, ext, n, 1.0, sdef);
   __syncthreads();
@@ -261,6 +260,12 @@ __device__ void line_drive_update(paqif_ehl_line_drive& d, double res, int fb, d
   if (d.outer >= d.max_outer) d.done = 3;
 }
 
+#ifdef PAQIF_LINE_PROF  // dev: phase cycles of case 0, printed per launch
+#define LINE_T(i) lt##i = clock64()
+#else
+#define LINE_T(i)
+#endif
+
 template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kEhlThreads, 1)
 ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
@@ -272,6 +277,9 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   extern __shared__ __align__(16) double esm[];
   const int64_t b = blockIdx.x;
   if (b >= B) return;
+#ifdef PAQIF_LINE_PROF
+  long long lt0 = 0, lt1 = 0, lt2 = 0, lt3 = 0, lt4 = 0, lt5 = 0, lt6 = 0, lt7 = 0;
+#endif
   int outer = c.outer;
   if (drv) {  // device-driven solve_ehl: stopped cases skip
     if (drv[b].done) return;
@@ -306,13 +314,14 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   double h0 = h0_io[b];
 
   for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
-  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
-    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  ext4_build(table, n, ext);
   __syncthreads();
 
+  LINE_T(0);
   // ---- film, rheology, faces, residual of the current pressure
   toeplitz_conv(su, ext, n, 1.0, sdef);
   __syncthreads();
+  LINE_T(1);
   double qmax = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     const double x = c.lo + h * (double)i;
@@ -343,6 +352,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   }
   __syncthreads();
 
+  LINE_T(2);
   // kernel sensitivities (film.sensitivity, sweeps.kernel_nu)
   const double s0 = sign * table[0], s1 = sign * table[1], s2 = sign * table[2];
   const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
@@ -381,6 +391,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     }
     if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
     __syncthreads();
+    LINE_T(3);
     // solve on warp 0 (aqif2: factor + fused W, Z outside-in)
     int* flag = reinterpret_cast<int*>(red + 30);
     st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, xsol, flag) & 1;
@@ -397,6 +408,7 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     return;
   }
 
+  LINE_T(4);
   // ---- update (solver.py:169-181)
   bool finite = true;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -419,9 +431,11 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     sun[i] = (i == 0 || i == n) ? 0.0 : np_maximum(0.0, v);
   }
   const int fin_all = __syncthreads_and(finite);
+  LINE_T(5);
   // ---- deformation of the new pressure, force balance, residual
   toeplitz_conv(sun, ext, n, 1.0, sdef);
   __syncthreads();
+  LINE_T(6);
   int fb = 0;
   double deficit_v = __longlong_as_double(0x7ff8000000000000ll);
   if ((outer + 1) % c.force_every == 0) {
@@ -449,6 +463,12 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
     if (drv) line_drive_update(drv[b], cmax / h, fb, deficit_v, fin_all, hist_res, hist_def,
                                hist_cap, b);
   }
+#ifdef PAQIF_LINE_PROF
+  LINE_T(7);
+  if (b == 0 && threadIdx.x == 0)
+    printf("[line_prof] n=%d conv1 %lld rheo/faces %lld assemble %lld solve(last rung) %lld update %lld conv2 %lld resid %lld rung %d\n",
+           n, lt1 - lt0, lt2 - lt1, lt3 - lt2, lt4 - lt3, lt5 - lt4, lt6 - lt5, lt7 - lt6, rung);
+#endif
 }
 
 }  // namespace paqif
@@ -528,10 +548,9 @@ line_deformation_kernel(int n, const double* __restrict__ table, const double* _
 {
   extern __shared__ __align__(16) double dsm[];
   const int N = n + 1;
-  double* ext = dsm + 8;
-  double* su = dsm + 2 * n + 1 + 16;
-  for (int k = threadIdx.x - 8; k < 2 * n + 1 + 8; k += blockDim.x)
-    ext[k] = (k >= 0 && k < 2 * n + 1) ? table[k >= n ? k - n : n - k] : 0.0;
+  double* ext = dsm;
+  double* su = dsm + ext4_doubles(n);
+  ext4_build(table, n, ext);
   for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u[(size_t)blockIdx.x * N + k];
   __syncthreads();
   toeplitz_conv(su, ext, n, -1.0 / 3.141592653589793, out + (size_t)blockIdx.x * N);
@@ -543,7 +562,7 @@ extern "C" int paqif_line_deformation(int64_t B, int64_t n, const double* table,
 {
   if (B < 0 || n < 1) return set_arg_error("line_deformation: bad sizes");
   if (B == 0) return PAQIF_OK;
-  const size_t smem = (size_t)(2 * n + 1 + 16 + n + 1 + 8) * 8;
+  const size_t smem = (size_t)(ext4_doubles((int)n) + n + 1 + 8) * 8;
   if (smem > 227 * 1024) return set_arg_error("line_deformation: grid too fine");
   cudaFuncSetAttribute(line_deformation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   line_deformation_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>((int)n, table, u, out);
