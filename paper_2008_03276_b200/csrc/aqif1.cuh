@@ -10,7 +10,7 @@
 // record in shared memory.  Arithmetic: the reference recurrence
 // (paqif/_kernels.py:62-225) at beta = 1 in the reference's operation order
 // -- bit for bit in EXACT mode identical to the general warp engine
-// (aqif_factor_group / zsolve_group with BETA = 1, tools/aqif2_check.cu).
+// (aqif_factor_group / zsolve_group with BETA = 1, tools/aqif1_check.cu).
 //
 // Record of level k (12 doubles): P_t.L[0..1], P_t.R[0..1], P_b.L[0..1],
 // P_b.R[0..1], y_t, y_b, det, 1/det; after the Z solve y_t, y_b hold
@@ -223,7 +223,8 @@ __device__ int aqif1_solve(const double* band, const double* rhs, int n, double*
     bool ok = aqif1_factor<EXACT, false>(band, rhs, n, rec, threadIdx.x);
     __syncwarp();
     bool bad = aqif1_breakdown(rec, n, 1e-14, threadIdx.x);
-    ok = aqif1_zsolve<EXACT, false>(rec, n, threadIdx.x) && ok;
+    // a certain breakdown (safe divisions) needs no Z solve
+    if (!(ok & bad)) ok = aqif1_zsolve<EXACT, false>(rec, n, threadIdx.x) && ok;
     if (!ok) {  // a division left the Markstein range: exact slow path
       __syncwarp();
       aqif1_factor<EXACT, true>(band, rhs, n, rec, threadIdx.x);

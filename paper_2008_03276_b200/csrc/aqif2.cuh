@@ -310,7 +310,9 @@ __device__ int aqif2_solve(const double* band, const double* rhs, int n, double*
     const long long c1 = clock64();
     const bool bad0 = aqif2_breakdown(rec, n, 1e-14, threadIdx.x);
     const long long c2 = clock64();
-    ok = aqif2_zsolve<EXACT, false>(rec, n, threadIdx.x) && ok;
+    // a certain breakdown (safe divisions) needs no Z solve: the caller
+    // discards the solution and tries the next rung
+    if (!(ok & bad0)) ok = aqif2_zsolve<EXACT, false>(rec, n, threadIdx.x) && ok;
     const long long c3 = clock64();
     bool bad = bad0;
     if (!ok) {  // a division left the Markstein range: exact slow path

@@ -266,17 +266,16 @@ __device__ void line_drive_update(paqif_ehl_line_drive& d, double res, int fb, d
 #define LINE_T(i)
 #endif
 
+// One outer iteration of case b; all threads of the CTA call (esm: the
+// CTA's dynamic shared memory).
 template <bool EXACT, bool SMEM>
-__global__ void __launch_bounds__(kEhlThreads, 1)
-ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
-                const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
-                double* h0_io, double* film_out, double* res_out, double* deficit_out,
-                int32_t* info_out, char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv,
-                double* hist_res, double* hist_def, int hist_cap)
+__device__ __forceinline__ void line_case(
+    const paqif_ehl_line_cfg& c, int64_t B, const double* __restrict__ table,
+    const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
+    double* h0_io, double* film_out, double* res_out, double* deficit_out, int32_t* info_out,
+    char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv, double* hist_res, double* hist_def,
+    int hist_cap, const int64_t b, double* esm)
 {
-  extern __shared__ __align__(16) double esm[];
-  const int64_t b = blockIdx.x;
-  if (b >= B) return;
 #ifdef PAQIF_LINE_PROF
   long long lt0 = 0, lt1 = 0, lt2 = 0, lt3 = 0, lt4 = 0, lt5 = 0, lt6 = 0, lt7 = 0;
 #endif
@@ -468,6 +467,56 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
   if (b == 0 && threadIdx.x == 0)
     printf("[line_prof] n=%d conv1 %lld rheo/faces %lld assemble %lld solve(last rung) %lld update %lld conv2 %lld resid %lld rung %d\n",
            n, lt1 - lt0, lt2 - lt1, lt3 - lt2, lt4 - lt3, lt5 - lt4, lt6 - lt5, lt7 - lt6, rung);
+
+#endif
+}
+
+// Grid = one CTA per SM pulling cases from a queue (`queue` non-null: the
+// order kernel resets it), in `order` -- the cases that needed the Ls4
+// ladder last time first, so the long ones start early and the rest fill
+// in behind them; or one CTA per case (queue null).
+template <bool EXACT, bool SMEM>
+__global__ void __launch_bounds__(kEhlThreads, 1)
+ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
+                const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
+                double* h0_io, double* film_out, double* res_out, double* deficit_out,
+                int32_t* info_out, char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv,
+                double* hist_res, double* hist_def, int hist_cap, const int32_t* order,
+                int* queue)
+{
+  extern __shared__ __align__(16) double esm[];
+  if (!queue) {
+    if ((int64_t)blockIdx.x >= B) return;
+    line_case<EXACT, SMEM>(c, B, table, p_hertz, lamv, u_io, h0_io, film_out, res_out,
+                           deficit_out, info_out, ws, ws_per_case, drv, hist_res, hist_def,
+                           hist_cap, (int64_t)blockIdx.x, esm);
+    return;
+  }
+  __shared__ int next;
+#ifdef PAQIF_LINE_PROF
+  unsigned long long g0, g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  const long long c0 = clock64();
+  int ncase = 0;
+#endif
+  for (;;) {
+    __syncthreads();  // the previous case is done with shared memory and `next`
+    if (threadIdx.x == 0) next = atomicAdd(queue, 1);
+    __syncthreads();
+    const int idx = next;
+    if (idx >= B) break;
+    line_case<EXACT, SMEM>(c, B, table, p_hertz, lamv, u_io, h0_io, film_out, res_out,
+                           deficit_out, info_out, ws, ws_per_case, drv, hist_res, hist_def,
+                           hist_cap, (int64_t)order[idx], esm);
+#ifdef PAQIF_LINE_PROF
+    ++ncase;
+#endif
+  }
+#ifdef PAQIF_LINE_PROF
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  if (threadIdx.x == 0)
+    printf("[cta] %d cases %d start_ns %llu end_ns %llu cycles %lld\n", blockIdx.x, ncase, g0, g1,
+           clock64() - c0);
 #endif
 }
 
@@ -475,17 +524,48 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
 
 using namespace paqif;
 
-extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
-  if (B < 0 || n < 4) return 0;
+namespace {
+// per-case workspace bytes: the line system when it does not fit in shared
+// memory (EhlSmemLayout), else a small pad
+size_t line_ws_per_case(int64_t n) {
   const int64_t n_int = n - 1;
   const int64_t n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
   const int64_t s = n_sys / 2;
-  // the line system lives in shared memory when it fits (EhlSmemLayout)
-  if (n <= (1 << 20) && EhlSmemLayout((int)n).sys_in_smem) return (size_t)B * 256;
+  if (n <= (1 << 20) && EhlSmemLayout((int)n).sys_in_smem) return 256;
   const size_t per = (aqif2_band_doubles((int)n_sys) + aqif2_rhs_doubles((int)n_sys) +
                       (size_t)(s + 1) * kRec2 + 32) * 8;
-  return (size_t)B * ((per + 255) & ~(size_t)255);
+  return (per + 255) & ~(size_t)255;
 }
+}  // namespace
+
+// B per-case areas, then the case order (B int32) and the queue counter
+extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
+  if (B < 0 || n < 4) return 0;
+  return (size_t)B * line_ws_per_case(n) + (((size_t)B * 4 + 4 + 255) & ~(size_t)255);
+}
+
+namespace paqif {
+// Case order for the next launch: the cases whose last step needed the Ls4
+// ladder (several line solves; info bits 0-1 or bit 8) first, so they start
+// in the first wave instead of trailing the last one.  Results do not depend
+// on the order (every case is independent); `info` may hold anything.
+__global__ void line_order_kernel(const int32_t* __restrict__ info, int64_t B, int32_t* order,
+                                  int* queue) {
+  __shared__ int lo, hi;
+  if (threadIdx.x == 0) {
+    lo = 0;
+    hi = 0;
+    *queue = 0;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
+    const int32_t v = info[i];
+    const bool slow = (v & 3) != 0 || (v & (1 << 8)) != 0;
+    if (slow) order[atomicAdd(&hi, 1)] = (int32_t)i;
+    else order[B - 1 - atomicAdd(&lo, 1)] = (int32_t)i;
+  }
+}
+}  // namespace paqif
 
 namespace {
 int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const double* table,
@@ -501,16 +581,27 @@ int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const d
   const EhlSmemLayout L(cfg->n);
   const size_t smem = (size_t)L.total * 8;
   if (smem > 227 * 1024) return set_arg_error("ehl_line: grid too fine for one CTA");
-  const size_t per = need / (size_t)B;
+  const size_t per = line_ws_per_case(cfg->n);
+  int32_t* order = reinterpret_cast<int32_t*>((char*)workspace + (size_t)B * per);
+  int* queue = reinterpret_cast<int*>(order + B);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool queued = B > sms;
   cudaStream_t st = (cudaStream_t)stream;
   auto kern = (flags & PAQIF_FLAG_EXACT)
                   ? (L.sys_in_smem ? ehl_line_kernel<true, true> : ehl_line_kernel<true, false>)
                   : (L.sys_in_smem ? ehl_line_kernel<false, true> : ehl_line_kernel<false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int32_t s = 0; s < steps; ++s)
-    kern<<<(unsigned)B, kEhlThreads, smem, st>>>(*cfg, B, table, p_hertz, lam, u, h0, film, res,
-                                                 deficit, info, (char*)workspace, per, drv,
-                                                 hist_res, hist_def, hist_cap);
+  for (int32_t s = 0; s < steps; ++s) {
+    if (queued) line_order_kernel<<<1, 1024, 0, st>>>(info, B, order, queue);
+    kern<<<(unsigned)(queued ? sms : B), kEhlThreads, smem, st>>>(
+        *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, (char*)workspace, per, drv,
+        hist_res, hist_def, hist_cap, queued ? order : nullptr, queued ? queue : nullptr);
+  }
   return check_launch(who);
 }
 }  // namespace
