@@ -296,24 +296,30 @@ __device__ __forceinline__ bool aqif2_breakdown(const double* rec, int n, double
 // band/rhs/x/rec in shared memory (x may alias band).  Returns bit 0 set on a
 // breakdown (the reference's FactorizationBreakdownError), bit 1 if the
 // checked repeat ran.
-// dev phase counters (cycles: factor, breakdown, z, gather; count), per TU
+// dev phase counters (cycles: factor, breakdown, z, gather; count), per TU;
+// only with -DPAQIF_DEV_PROF (PAQIF_NVCC_EXTRA), read by PAQIF_PT_PROF=1
 __device__ unsigned long long g_aqif2_prof[8];
+#ifdef PAQIF_DEV_PROF
+#define AQ2_T(v) const long long v = clock64()
+#else
+#define AQ2_T(v)
+#endif
 
 template <bool EXACT>
 __device__ int aqif2_solve(const double* band, const double* rhs, int n, double* rec, double* x,
                            int* flag_smem) {
   __syncthreads();
   if (threadIdx.x < 32) {
-    const long long c0 = clock64();
+    AQ2_T(c0);
     bool ok = aqif2_factor<EXACT, false>(band, rhs, n, rec, threadIdx.x);
     __syncwarp();
-    const long long c1 = clock64();
+    AQ2_T(c1);
     const bool bad0 = aqif2_breakdown(rec, n, 1e-14, threadIdx.x);
-    const long long c2 = clock64();
+    AQ2_T(c2);
     // a certain breakdown (safe divisions) needs no Z solve: the caller
     // discards the solution and tries the next rung
     if (!(ok & bad0)) ok = aqif2_zsolve<EXACT, false>(rec, n, threadIdx.x) && ok;
-    const long long c3 = clock64();
+    AQ2_T(c3);
     bool bad = bad0;
     if (!ok) {  // a division left the Markstein range: exact slow path
       __syncwarp();
@@ -326,12 +332,14 @@ __device__ int aqif2_solve(const double* band, const double* rhs, int n, double*
     aqif2_gather(rec, n, x, threadIdx.x);
     if (threadIdx.x == 0) {
       *flag_smem = (bad ? 1 : 0) | (ok ? 0 : 2);
+#ifdef PAQIF_DEV_PROF
       const long long c4 = clock64();
       atomicAdd(&g_aqif2_prof[0], (unsigned long long)(c1 - c0));
       atomicAdd(&g_aqif2_prof[1], (unsigned long long)(c2 - c1));
       atomicAdd(&g_aqif2_prof[2], (unsigned long long)(c3 - c2));
       atomicAdd(&g_aqif2_prof[3], (unsigned long long)(c4 - c3));
       atomicAdd(&g_aqif2_prof[4], 1ull);
+#endif
     }
   }
   __syncthreads();
