@@ -78,6 +78,9 @@ __device__ __forceinline__ double np_min(double a, double b) {
 }
 
 constexpr int kLcpWarpsPerBlock = 4;
+#ifndef PAQIF_LCP_MINB
+#define PAQIF_LCP_MINB 2  // resident blocks per SM the register budget is sized for
+#endif
 
 #ifdef PAQIF_PROFILE_PHASES
 // dev-only phase timers (tools/phase_prof.cu): factor, corner, zsolve, check
@@ -208,7 +211,7 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
 }
 
 template <int BETA, bool EXACT, bool SOLVE_ONLY>
-__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, 2)
+__global__ void __launch_bounds__(32 * kLcpWarpsPerBlock, PAQIF_LCP_MINB)
 lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __restrict__ f,
            double tol, int max_outer, double* u_out, uint8_t* act_out, int64_t* passes_out,
            double* res_out, int64_t* status_out, char* ws, size_t ws_per_slot, int total_warps,
