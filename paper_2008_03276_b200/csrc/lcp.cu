@@ -253,7 +253,6 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
     const double* fb = f + (have ? b : 0) * (size_t)n;
     double* ub = u_out + (have ? b : 0) * (size_t)n;
     uint8_t* ab = SOLVE_ONLY ? nullptr : act_out + (have ? b : 0) * (size_t)n;
-    double cmax = 0.0, fmax = 0.0;
     if (have) {
       for (int i = gl; i < n; i += G) {
         const double fi = fb[i];
@@ -262,20 +261,9 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         if (!SOLVE_ONLY) {
           ub[i] = 0.0;
           ab[i] = (uint8_t)a;
-          double c = 0.0;
-          for (int d = 0; d <= 2 * BETA; ++d) c = c + fabs(bd[(size_t)d * n + i]);
-          cmax = c > cmax ? c : cmax;
-          fmax = fabs(fi) > fmax ? fabs(fi) : fmax;
         }
       }
     }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      cmax = fmax_(cmax, __shfl_xor_sync(FULL, cmax, o));
-      fmax = fmax_(fmax, __shfl_xor_sync(FULL, fmax, o));
-    }
-    const double floor_ = 1e3 * DBL_EPSILON * (cmax + fmax);
-    const double lim = tol > floor_ ? tol : floor_;
     double best_res = INFINITY, res = INFINITY;
     int passes = 0, st = 0;
     bool done = false;
@@ -391,7 +379,20 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       if (!active) continue;
       res = r;
       if (res <= tol || res < best_res) {
-        for (int i = gl; i < n; i += G) {
+        int i = gl;
+        for (; i + 3 * G < n; i += 4 * G) {  // loads of four rows in flight
+          const double x0 = x[i], x1 = x[i + G], x2 = x[i + 2 * G], x3 = x[i + 3 * G];
+          const uint32_t c0 = cur[i], c1 = cur[i + G], c2 = cur[i + 2 * G], c3 = cur[i + 3 * G];
+          ub[i] = np_max0(x0);
+          ub[i + G] = np_max0(x1);
+          ub[i + 2 * G] = np_max0(x2);
+          ub[i + 3 * G] = np_max0(x3);
+          ab[i] = (uint8_t)c0;
+          ab[i + G] = (uint8_t)c1;
+          ab[i + 2 * G] = (uint8_t)c2;
+          ab[i + 3 * G] = (uint8_t)c3;
+        }
+        for (; i < n; i += G) {
           ub[i] = np_max0(x[i]);
           ab[i] = (uint8_t)cur[i];
         }
@@ -410,9 +411,29 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       cur = nxt;
       nxt = t;
     }
-    if (have && !done && st == 0) {
-      if (best_res <= lim) res = best_res;
-      else st = PAQIF_LCP_NONCONVERGED;
+    if (__any_sync(FULL, have && !done && st == 0)) {
+      // acceptance floor of a system that did not converge
+      // (parallel.py:344-347): 1e3 eps (max row sum |L| + max |f|), only
+      // needed here, so the band is not read for it otherwise
+      double cmax = 0.0, fmax = 0.0;
+      if (!SOLVE_ONLY && have && !done && st == 0)
+        for (int i = gl; i < n; i += G) {
+          double c = 0.0;
+          for (int d = 0; d <= 2 * BETA; ++d) c = c + fabs(bd[(size_t)d * n + i]);
+          cmax = c > cmax ? c : cmax;
+          fmax = fabs(fb[i]) > fmax ? fabs(fb[i]) : fmax;
+        }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) {
+        cmax = fmax_(cmax, __shfl_xor_sync(FULL, cmax, o));
+        fmax = fmax_(fmax, __shfl_xor_sync(FULL, fmax, o));
+      }
+      const double floor_ = 1e3 * DBL_EPSILON * (cmax + fmax);
+      const double lim = tol > floor_ ? tol : floor_;
+      if (have && !done && st == 0) {
+        if (best_res <= lim) res = best_res;
+        else st = PAQIF_LCP_NONCONVERGED;
+      }
     }
     __syncwarp();
     if (have && gl == 0) {
