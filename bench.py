@@ -193,9 +193,11 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
 
     p1 = _line_params(20.0, 10.0)
     ms1 = timed(LineContactBatch([p1], 512), steps1)
+    ms1f = timed(LineContactBatch([p1], 512, exact=False), steps1)
     out["config1"] = {"metric": "EHL Newton iters/s (line, N=513, M=20, L=10, B=1)",
                       "value": 1e3 / ms1, "unit": "iters/s", "us_per_iter": ms1 * 1e3,
-                      "gpu_launches_per_iter": 1}
+                      "gpu_launches_per_iter": 1,
+                      "fma": {"us_per_iter": ms1f * 1e3, "value": 1e3 / ms1f}}
     # end to end through the public solve_ehl (device-side stop tests, one
     # host synchronisation per 32 iterations; initial state uploaded, final
     # state read back inside the timed region)
@@ -216,10 +218,13 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
     b3 = LineContactBatch([_line_params(m, l) for m, l in cases], 1024)
     ms3 = timed(b3, steps3)
     info = b3.info.cpu().numpy()
+    ms3f = timed(LineContactBatch([_line_params(m, l) for m, l in cases], 1024, exact=False),
+                 steps3)
     out["config3"] = {"metric": "EHL line-contact case-iterations/s (1024 cases/GPU, N=1025)",
                       "value": world * len(cases) * 1e3 / ms3, "unit": "case-iters/s",
                       "ms_per_iter": ms3, "scaling": "weak",
-                      "ladder_cases_last_iter": int(np.sum((info & 3) > 0))}
+                      "ladder_cases_last_iter": int(np.sum((info & 3) > 0)),
+                      "fma": {"ms_per_iter": ms3f, "value": world * len(cases) * 1e3 / ms3f}}
     if with_cpu:
         import oracle.ehl_oracle as E
         c = E.LineCase(p_hertz=p1.p_hertz, lam=p1.lam)
@@ -247,6 +252,8 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
                                           "cores": 1, "kind": "port",
                                           "sample": f"{k} oracle steps of case 0, one core"}
     out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
+    for v in out.values():
+        v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
     return out
 
 
@@ -258,9 +265,9 @@ def point_secondary(with_cpu, steps4=3, steps5=1):
     from paper_2008_03276_b200.ehl import EhlParams, PointContact
     out = {}
 
-    def run(n, m, steps, warm):
+    def run(n, m, steps, warm, exact=True):
         p = EhlParams.point_from_moes(m, 10.0, domain=(-4.5, 1.5), lo_y=-3.0)
-        pc = PointContact(p, n)
+        pc = PointContact(p, n, exact=exact)
         for _ in range(warm):
             pc.step()
         pc.sync()
@@ -283,6 +290,9 @@ def point_secondary(with_cpu, steps4=3, steps5=1):
                           "value": 1e3 / ms4, "unit": "iters/s", "ms_per_iter": ms4,
                           "lines_per_iter": 2 * 511, "newton_x_lines_last": int(s4["newton"].sum()),
                           "residual_last": s4["res"]}
+        ms4f, s4f = run(512, 100.0, steps4, 3, exact=False)
+        out["config4"]["fma"] = {"ms_per_iter": ms4f, "value": 1e3 / ms4f,
+                                 "newton_x_lines_last": int(s4f["newton"].sum())}
         if with_cpu:
             import oracle.ehl_point_oracle as P
             c = P.point_case(100.0, 10.0)
@@ -298,6 +308,8 @@ def point_secondary(with_cpu, steps4=3, steps5=1):
         out["config5"] = {"metric": "EHL point Newton iters/s (2049x2049, M=1000, L=10)",
                           "value": 1e3 / ms5, "unit": "iters/s", "ms_per_iter": ms5,
                           "lines_per_iter": 2 * 2047, "residual_last": s5["res"]}
+    for v in out.values():
+        v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
     return out
 
 
