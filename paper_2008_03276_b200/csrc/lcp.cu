@@ -361,8 +361,19 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         };
         // rows in order (the NaN-propagating max is order independent),
         // two per step so twice the loads are in flight
+        // prefetch into L1 the band lines of the next step's rows (2 x 16
+        // rows x 17 diagonals = 34 lines of 128 B; about 2 per lane) so its
+        // loads hit L1 instead of waiting on DRAM
+        auto prefetch_rows = [&](int r0) {
+          for (int q = gl; q < 2 * (2 * BETA + 1); q += G) {
+            const int d = q >> 1, rr = r0 + (q & 1) * G;
+            if (rr < n)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(bd + (size_t)d * n + rr));
+          }
+        };
         int i = gl;
         for (; i + G < n; i += 2 * G) {
+          prefetch_rows(i - gl + 4 * G);
           row(i);
           row(i + G);
         }
