@@ -99,6 +99,51 @@ int paqif_line_deformation(int64_t B, int64_t n, const double *table /*[dev] n+1
                            const double *u /*[dev] (B, n+1)*/, double *out /*[dev] (B, n+1)*/,
                            void *stream);
 
+/* ------------------------------------------------------- line systems
+ * The per-line building blocks of paqif/ehl/sweeps.py on the GPU, for
+ * callers that work line by line with the reference's arrays ([dev]
+ * pointers, one CTA per call). */
+typedef struct {
+  int32_t n;        /* intervals: nodes n + 1, unknowns n - 1               */
+  int32_t limiter;  /* 0 kappa, 1 none, 2 van-albada, 3 minmod, 4 koren    */
+  int32_t weighted; /* 1: Ls4/Ls5 distributive pattern, 0: Ls1/Ls0         */
+  int32_t reserved;
+  double kappa;
+  double ks0, ks1;  /* kernel strengths (film sensitivity x kernel_nu,
+                       sweeps.py:190-199, computed by the caller)          */
+  double h, hy;     /* spacing; hy = h (point contact) or 1 (line)         */
+  const double *q, *rho;                              /* [dev] n + 1       */
+  const double *ex_p, *ex_m, *ey_p, *ey_m, *resid;    /* [dev] n - 1       */
+} paqif_ehl_linesys;
+
+/* assemble_line_system (ehl/sweeps.py:157-267; splitting_ls4/ls5 are the
+ * weighted pattern): the padded change matrix of order n_sys (n - 1 rounded
+ * up to even) in BandedMatrix layout bands[(d + 2) * n_sys + i] (beta = 2)
+ * and its right side rhs[n_sys].  jacobian: 0 scheme, 1 first-order,
+ * 2 diagonal. */
+int paqif_ehl_assemble_line(const paqif_ehl_linesys *a, int32_t jacobian,
+                            double *bands /*[dev] 5 x n_sys*/, double *rhs /*[dev] n_sys*/,
+                            void *stream);
+
+/* robust_line_solve (ehl/sweeps.py:270-295): scheme, first-order, diagonal
+ * Jacobians until the AQIF factorization succeeds; sigma[n - 1] and the rung
+ * that solved (-1: every rung broke down, the reference re-raises). */
+int paqif_ehl_robust_line_solve(const paqif_ehl_linesys *a, double *sigma /*[dev] n-1*/,
+                                int32_t *rung /*[dev] 1*/, void *stream);
+
+typedef struct {
+  int32_t compressible;
+  int32_t reserved;
+  double alpha, z, p0, p_hertz, lam;
+} paqif_ehl_rheo;
+
+/* reynolds_residual_field (ehl/sweeps.py:106-138): the residual of the
+ * discrete balance on every interior node, boundary entries zero; u and
+ * film are (n+1) (point = 0) or (n+1) x (n+1) (point = 1). */
+int paqif_ehl_residual_field(const double *u, const double *film, int64_t n, int32_t point,
+                             const paqif_ehl_rheo *rheo, double h, int32_t limiter,
+                             double kappa, double *r, void *stream);
+
 /* ------------------------------------------------------------ point contact
  * One outer iteration of ehl.solver.solve_ehl for the circular point contact
  * (configs 4/5) on an (n+1)^2 grid, in the reference's Gauss-Seidel order:

@@ -22,7 +22,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"] + ARCH
 
-SOURCES = ["dropin.cu", "lcp.cu", "version.cu", "ehl_line.cu", "ehl_point.cu", "rblock.cu"]
+SOURCES = ["dropin.cu", "lcp.cu", "version.cu", "ehl_line.cu", "ehl_point.cu", "rblock.cu",
+           "ehl_linesys.cu"]
 
 
 def _nvcc() -> str:

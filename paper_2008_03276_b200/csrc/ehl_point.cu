@@ -256,57 +256,8 @@ __device__ __forceinline__ void point_row(double rw, double rc, double re, doubl
                                           double ex_m, double ey_p, double ey_m, double phi_p,
                                           double phi_m, double h, bool weighted, int jac,
                                           double ks0, double ks1, double* e) {
-  if (jac != 0) {
-    phi_p = 0.0;
-    phi_m = 0.0;
-  }
-  const double a_p = 1.0 - 0.5 * phi_p, b_p = 0.5 * phi_p;
-  const double a_m = 1.0 - 0.5 * phi_m, b_m = 0.5 * phi_m;
-  const double hy = h;
-  double c_m2, c_m1, c_0, c_p1, c_p2;
-  if (jac == 2) {
-    c_m2 = 0.0; c_m1 = 0.0; c_p1 = 0.0; c_p2 = 0.0;
-    c_0 = -hy * rc * fabs(ks0);
-  } else {
-    c_m2 = hy * (a_m * rw * ks1);
-    c_m1 = -hy * (a_p * rc * ks1 - a_m * rw * ks0 - b_m * rc * ks1);
-    c_0 = -hy * (a_p * rc * ks0 + b_p * re * ks1 - a_m * rw * ks1 - b_m * rc * ks0);
-    c_p1 = -hy * (a_p * rc * ks1 + b_p * re * ks0 - b_m * rc * ks1);
-    c_p2 = -hy * (b_p * re * ks1);
-  }
-  const double ey_sum = ey_p + ey_m;
-  double p_m2, p_m1, p_0, p_p1, p_p2;
-  if (weighted) {
-    p_m2 = -0.25 * ex_m / h;
-    p_m1 = (1.25 * ex_m + 0.25 * ex_p) / h + 0.25 * ey_sum / h;
-    p_0 = -1.25 * (ex_p + ex_m + ey_sum) / h;
-    p_p1 = (1.25 * ex_p + 0.25 * ex_m) / h + 0.25 * ey_sum / h;
-    p_p2 = -0.25 * ex_p / h;
-  } else {
-    p_m2 = 0.0;
-    p_m1 = ex_m / h;
-    p_0 = -(ex_p + ex_m + ey_sum) / h;
-    p_p1 = ex_p / h;
-    p_p2 = 0.0;
-  }
-  e[0] = -(c_m2 + p_m2);
-  e[1] = -(c_m1 + p_m1);
-  e[2] = -(c_0 + p_0);
-  e[3] = -(c_p1 + p_p1);
-  e[4] = -(c_p2 + p_p2);
-  const double off_mag = fabs(e[0]) + fabs(e[1]) + fabs(e[3]) + fabs(e[4]);
-  const double floor_ = 0.05 * hy * fabs(rc) * fabs(ks0);
-  if (fabs(e[2]) < np_maximum(0.2 * off_mag, floor_)) {
-    const double fo_m2 = hy * rw * ks1;
-    const double fo_m1 = -hy * (rc * ks1 - rw * ks0);
-    const double fo_0 = -hy * (rc * ks0 - rw * ks1);
-    const double fo_p1 = -hy * rc * ks1;
-    e[0] = -(fo_m2 + p_m2);
-    e[1] = -(fo_m1 + p_m1);
-    e[2] = -(fo_0 + p_0);
-    e[3] = -(fo_p1 + p_p1);
-    e[4] = -p_p2;
-  }
+  line_row_entries(rw, rc, re, ex_p, ex_m, ey_p, ey_m, phi_p, phi_m, h, h, weighted, jac, ks0,
+                   ks1, e);
 }
 
 // worst |resid| of the sweep (python max over lines ignores NaN lines)
