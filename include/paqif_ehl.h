@@ -217,6 +217,20 @@ int paqif_ehl_point_sync(paqif_ehl_point *h);
 /* The handle's CUDA stream (cudaStream_t), for event timing and ordering. */
 void *paqif_ehl_point_stream(paqif_ehl_point *h);
 
+/* FilmModel.note_line_update (ehl/film.py:83-91): record an applied line
+ * change -- axis 0 row / 1 column at `index`, delta [host] (n+1) -- as a
+ * pending update; an all-zero delta is ignored.  At most 9 may be pending:
+ * the caller folds (paqif_ehl_point_deformation clears the list) once more
+ * than 8 are, as the reference does. */
+int paqif_ehl_point_note_update(paqif_ehl_point *h, int32_t axis, int32_t index,
+                                const double *delta);
+
+/* FilmModel.film_rows / film_cols (ehl/film.py:125-146): h0 + geometry +
+ * base deformation + pending corrections on L lines (mode 0 rows, 1
+ * columns; indices idx [host] L) -> out [host] L x (n+1). */
+int paqif_ehl_point_film_lines(paqif_ehl_point *h, int32_t mode, const int32_t *idx, int32_t L,
+                               double h0, double *out);
+
 /* Deformation of HOST pressure u into HOST out (FilmModel.deformation_full). */
 int paqif_ehl_point_deformation(paqif_ehl_point *h, const double *u, double *out);
 

@@ -1148,8 +1148,60 @@ extern "C" int paqif_ehl_point_deformation(paqif_ehl_point* h, const double* u, 
   const size_t NN = (size_t)h->d.N * h->d.N;
   cudaMemcpyAsync(h->d.film_out, u, NN * 8, cudaMemcpyHostToDevice, h->st);
   pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
-  fft_deformation(h->plan, h->d.film_out, h->d.dbase, &h->d.meta[kMGate], nullptr, h->st);
-  cudaMemcpyAsync(out, h->d.dbase, NN * 8, cudaMemcpyDeviceToHost, h->st);
+  // deformation_full: fresh base, pending line updates cleared (film.py:67-79)
+  fft_deformation(h->plan, h->d.film_out, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount],
+                  h->st);
+  if (out) cudaMemcpyAsync(out, h->d.dbase, NN * 8, cudaMemcpyDeviceToHost, h->st);
   cudaError_t e = cudaStreamSynchronize(h->st);
   return e == cudaSuccess ? check_launch("ehl_point_deformation") : set_cuda_error("deformation", e);
 }
+
+namespace paqif {
+// append a pending line update (FilmModel.note_line_update)
+__global__ void pt_note_kernel(PointDev d, int axis, int index, const double* __restrict__ delta) {
+  const int p = d.meta[kMCount];
+  if (p >= kMaxPending) return;  // the caller folds before this can happen
+  for (int i = threadIdx.x; i < d.N; i += blockDim.x) d.pend[(size_t)p * d.N + i] = delta[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d.meta[kMAxis + p] = axis;
+    d.meta[kMIdx + p] = index;
+    d.meta[kMCount] = p + 1;
+  }
+}
+}  // namespace paqif
+
+extern "C" int paqif_ehl_point_note_update(paqif_ehl_point* h, int32_t axis, int32_t index,
+                                           const double* delta) {
+  if (!h || !delta || axis < 0 || axis > 1 || index < 0 || index > h->d.n)
+    return set_arg_error("ehl_point_note_update");
+  bool any = false;
+  for (int i = 0; i < h->d.N; ++i) any |= delta[i] != 0.0;
+  if (!any) return PAQIF_OK;  // film.py:86-87
+  int count = 0;
+  cudaMemcpy(&count, &h->d.meta[kMCount], sizeof(int), cudaMemcpyDeviceToHost);
+  if (count >= kMaxPending) return set_arg_error("ehl_point_note_update: fold first (> 8 pending)");
+  // stage delta in the films buffer's rho half (4N spare doubles)
+  double* tmp = h->d.rcache + 4 * (size_t)h->d.N;
+  cudaMemcpyAsync(tmp, delta, (size_t)h->d.N * 8, cudaMemcpyHostToDevice, h->st);
+  pt_note_kernel<<<1, 256, 0, h->st>>>(h->d, axis, index, tmp);
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? check_launch("ehl_point_note_update") : set_cuda_error("note_update", e);
+}
+
+extern "C" int paqif_ehl_point_film_lines(paqif_ehl_point* h, int32_t mode, const int32_t* idx,
+                                          int32_t L, double h0, double* out) {
+  if (!h || !idx || !out || L < 0 || mode < 0 || mode > 1)
+    return set_arg_error("ehl_point_film_lines");
+  for (int k = 0; k < L; ++k)
+    if (idx[k] < 0 || idx[k] > h->d.n) return set_arg_error("ehl_point_film_lines: index");
+  const int N = h->d.N;
+  cudaMemcpyAsync(&h->d.scal[0], &h0, sizeof(double), cudaMemcpyHostToDevice, h->st);
+  for (int k = 0; k < L; ++k) {
+    films(h, mode, idx[k], 1, nullptr, h->d.films, h->d.rcache, 4 * (size_t)N);
+    cudaMemcpyAsync(out + (size_t)k * N, h->d.films, (size_t)N * 8, cudaMemcpyDeviceToHost, h->st);
+  }
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? check_launch("ehl_point_film_lines") : set_cuda_error("film_lines", e);
+}
+

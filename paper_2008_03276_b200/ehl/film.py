@@ -58,6 +58,42 @@ class FilmModel:
     def film_full(self, u, h0: float) -> np.ndarray:
         return h0 + self.geometry + self.deformation_full(u)
 
+    # -- pending line updates (film.py:83-146): the device keeps the list
+    # and applies the exact corrections (csrc/ehl_point.cu pt_films) --------
+
+    FOLD_LIMIT = 8
+
+    def note_line_update(self, axis: str, index: int, delta, u) -> None:
+        """Record an applied line change; fold into the base once more than
+        8 are pending."""
+        if axis not in ("row", "col"):
+            raise ContractViolationError(f"unknown axis {axis!r}")
+        delta = np.asarray(delta, dtype=np.float64)
+        if not np.any(delta):
+            return
+        if self.contact == "point":
+            if self._base is None:
+                raise ContractViolationError("call deformation_full first")
+            self._device.note_update(0 if axis == "row" else 1, index, delta)
+        self._pending.append((axis, int(index)))
+        if len(self._pending) > self.FOLD_LIMIT:
+            self.deformation_full(u)
+
+    def _lines(self, mode: int, idx, h0: float) -> np.ndarray:
+        if self._base is None:
+            raise ContractViolationError("call deformation_full first")
+        if self.contact == "line":
+            raise ContractViolationError("line contact has a single row")
+        return self._device.film_lines(mode, list(idx), h0)
+
+    def film_rows(self, rows, h0: float) -> np.ndarray:
+        """Current film on the requested rows (pending updates included)."""
+        return self._lines(0, rows, h0)
+
+    def film_cols(self, cols, h0: float) -> np.ndarray:
+        """Current film on the requested columns (pending updates included)."""
+        return self._lines(1, cols, h0)
+
     def sensitivity(self, d: int, axis_offset: int = 0) -> float:
         if self.contact == "line":
             return self.sign * float(self.kernel.table[abs(d)])

@@ -65,6 +65,11 @@ def _bind(L):
     L.paqif_ehl_point_residual.restype = ctypes.c_int
     L.paqif_ehl_point_deformation.argtypes = [vp, vp, vp]
     L.paqif_ehl_point_deformation.restype = ctypes.c_int
+    L.paqif_ehl_point_note_update.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp]
+    L.paqif_ehl_point_note_update.restype = ctypes.c_int
+    L.paqif_ehl_point_film_lines.argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int32,
+                                             ctypes.c_double, vp]
+    L.paqif_ehl_point_film_lines.restype = ctypes.c_int
     L._ehl_point_bound = True
     return L
 
@@ -135,6 +140,24 @@ class PointDevice:
         out = np.empty_like(uu)
         rc = self.h.L.paqif_ehl_point_deformation(self.h.ptr, _ptr(uu), _ptr(out))
         _native.check(rc, "paqif_ehl_point_deformation")
+        return out
+
+    def note_update(self, axis: int, index: int, delta) -> None:
+        """Append a pending line update (device list; see FilmModel)."""
+        dd = np.ascontiguousarray(delta, dtype=np.float64)
+        if dd.shape != (self.n + 1,):
+            raise ContractViolationError("delta must have n+1 entries")
+        rc = self.h.L.paqif_ehl_point_note_update(self.h.ptr, int(axis), int(index), _ptr(dd))
+        _native.check(rc, "paqif_ehl_point_note_update")
+
+    def film_lines(self, mode: int, idx, h0: float) -> np.ndarray:
+        """Films of rows (mode 0) / columns (mode 1) idx with the pending
+        corrections."""
+        ii = np.ascontiguousarray(idx, dtype=np.int32).reshape(-1)
+        out = np.empty((ii.size, self.n + 1))
+        rc = self.h.L.paqif_ehl_point_film_lines(self.h.ptr, int(mode), ii.ctypes.data,
+                                                 int(ii.size), float(h0), _ptr(out))
+        _native.check(rc, "paqif_ehl_point_film_lines")
         return out
 
 

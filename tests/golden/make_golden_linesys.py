@@ -10,8 +10,9 @@ Point-contact lines come from recorded states of ehl_point.npz through the
 reference's own _line_quantities (x-line j: films with pending corrections,
 rheology, face mobilities, residual); line-contact lines from states of
 ehl_line.npz with the same quantities the reference's _line_contact_sweep
-forms (ey = 0).  Every case stores its inputs, so the GPU test needs no
-reference.
+forms (ey = 0); FilmModel pending-update sequences (note_line_update,
+film_rows / film_cols, the fold past 8 pending).  Every case stores its
+inputs, so the GPU test needs no reference.
 """
 
 from __future__ import annotations
@@ -98,6 +99,48 @@ def main():
                               u_line=st.u, q_line=q_line, rho_line=rho, ex_p=ex_p, ex_m=ex_m,
                               ey_p=zeros, ey_m=zeros, resid=resid, bands=mat.bands, rhs=rhs,
                               sigma=sigma, u=st.u, film=film, field=field))
+    # FilmModel pending line updates: note rows / columns, read films of
+    # rows and columns with the exact corrections, then past the fold limit
+    rng = np.random.default_rng(5)
+    for name, key in (("f_e1", "e1"), ("f_e5", "e5")):
+        m, l, n, _ = GP[f"{key}__meta"]
+        n = int(n)
+        p = ref_params.EhlParams.point_from_moes(float(m), float(l), domain=(-4.5, 1.5))
+        st = adapted_state(p, n)
+        u = GP[f"{key}__u_in"].copy()
+        h0 = float(GP[f"{key}__h0_in"])
+        fm = st.film
+        fm.deformation_full(u)
+        notes, reads = [], []
+        plan = [("row", n // 2), ("row", n // 2 + 1), ("col", n // 3), ("row", 3),
+                ("col", n - 2)]
+        for axis, idx in plan:
+            delta = np.zeros(n + 1)
+            delta[1:n] = 1e-2 * rng.standard_normal(n - 1)
+            fm.note_line_update(axis, idx, delta, u)
+            notes.append((0 if axis == "row" else 1, idx, delta))
+        rows = [n // 2 - 1, n // 2, n // 2 + 1, 7]
+        cols = [n // 3 - 1, n // 3, n - 2]
+        reads.append((0, rows, fm.film_rows(rows, h0)))
+        reads.append((1, cols, fm.film_cols(cols, h0)))
+        zero = np.zeros(n + 1)
+        fm.note_line_update("row", 5, zero, u)  # ignored
+        for k in range(5):  # past the fold limit (9 > 8 folds)
+            delta = np.zeros(n + 1)
+            delta[1:n] = 1e-2 * rng.standard_normal(n - 1)
+            fm.note_line_update("row", 10 + k, delta, u)
+            notes.append((0, 10 + k, delta))
+        reads.append((0, rows, fm.film_rows(rows, h0)))
+        out[f"{name}__src"] = np.array(key)
+        out[f"{name}__u"] = u
+        out[f"{name}__h0"] = np.array(h0)
+        out[f"{name}__note_axis"] = np.array([a for a, _, _ in notes])
+        out[f"{name}__note_idx"] = np.array([i for _, i, _ in notes])
+        out[f"{name}__note_delta"] = np.stack([d for _, _, d in notes])
+        for q, (mode, idx, val) in enumerate(reads):
+            out[f"{name}__read{q}_mode"] = np.array(mode)
+            out[f"{name}__read{q}_idx"] = np.array(idx)
+            out[f"{name}__read{q}_val"] = val
     np.savez_compressed(os.path.join(HERE, "ehl_linesys.npz"), **out)
     print("wrote", len(POINT_CASES) + len(LINE_CASES), "cases")
 

@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 S = load_golden("ehl_linesys.npz")
 GP = load_golden("ehl_point.npz")
 GL = load_golden("ehl_line.npz")
-NAMES = sorted({k.split("__")[0] for k in S.files})
+NAMES = sorted({k.split("__")[0] for k in S.files if not k.startswith("f_")})
+FILMS = sorted({k.split("__")[0] for k in S.files if k.startswith("f_")})
 
 
 def case(name):
@@ -104,3 +105,35 @@ def test_contract_errors():
                                     jacobian="bogus")
     with pytest.raises(ContractViolationError):
         sweeps.assemble_line_system(*args(d), p, 1.0 / 3.0, "kappa", "Ls9", fm, float(d["h"]))
+
+
+@pytest.mark.parametrize("name", FILMS)
+def test_film_pending_updates(name):
+    """FilmModel.note_line_update / film_rows / film_cols on the device list
+    of pending line updates (exact corrections, fold past 8 pending) vs the
+    reference's sequence."""
+    from paper_2008_03276_b200.ehl import EhlParams, FilmModel
+    d = case(name)
+    m, l, n, _ = GP[f"{str(d['src'])}__meta"]
+    n = int(n)
+    p = EhlParams.point_from_moes(float(m), float(l), domain=(-4.5, 1.5), lo_y=-3.0)
+    h = (p.domain[1] - p.domain[0]) / n
+    fm = FilmModel("point", n, h, p.domain[0], lo_y=-3.0)
+    u, h0 = d["u"], float(d["h0"])
+    with pytest.raises(Exception):
+        fm.film_rows([1], h0)  # before deformation_full
+    fm.deformation_full(u)
+
+    def check(q):
+        mode, idx, val = int(d[f"read{q}_mode"]), list(d[f"read{q}_idx"]), d[f"read{q}_val"]
+        got = fm.film_rows(idx, h0) if mode == 0 else fm.film_cols(idx, h0)
+        assert rel(got, val) <= 1e-12
+
+    axes, idxs, deltas = d["note_axis"], d["note_idx"], d["note_delta"]
+    for k in range(len(axes)):
+        fm.note_line_update("row" if axes[k] == 0 else "col", int(idxs[k]), deltas[k], u)
+        if k == 4:
+            check(0)
+            check(1)
+            fm.note_line_update("row", 5, np.zeros(n + 1), u)  # ignored
+    check(2)
