@@ -34,6 +34,9 @@
 namespace paqif {
 
 constexpr int kRec2 = 16;
+// dev counters (-DPAQIF_DEV_PROF): [0..3] phase cycles, [4] solves,
+// [5] factor levels, [6] levels with a numerator below the Markstein range
+__device__ unsigned long long g_aqif2_prof[8];
 
 // Band storage: diagonal-major with kBandPad zero entries before and after
 // every diagonal (and around the right side), so the level loop reads rows
@@ -165,6 +168,17 @@ __device__ bool aqif2_factor(const double* __restrict__ band, const double* __re
     safe = safe & ds;
     const double wm = level_div<EXACT, CHECKED>(nm, det, y, ds, safe);
     const double wx = level_div<EXACT, CHECKED>(no, det, y, ds, safe);
+#ifdef PAQIF_DEV_PROF
+    {
+      const unsigned em = ((unsigned)__double2hiint(nm) >> 20) & 0x7ffu;
+      const unsigned ex = ((unsigned)__double2hiint(no) >> 20) & 0x7ffu;
+      const bool any_tiny = __any_sync(0xffffffffu, (em < 524u) | (ex < 524u));
+      if (lane_id == 0) {
+        atomicAdd(&g_aqif2_prof[5], 1ull);
+        if (any_tiny) atomicAdd(&g_aqif2_prof[6], 1ull);
+      }
+    }
+#endif
     const bool ok = (unsigned)row < (unsigned)n;
     const bool up = ok & !(is_zero(wm) & is_zero(wx));  // bitwise: no branches
     const double u1 = A::rank2(wo[1], wm, po[1], wx, oo[1]);
@@ -298,7 +312,6 @@ __device__ __forceinline__ bool aqif2_breakdown(const double* rec, int n, double
 // checked repeat ran.
 // dev phase counters (cycles: factor, breakdown, z, gather; count), per TU;
 // only with -DPAQIF_DEV_PROF (PAQIF_NVCC_EXTRA), read by PAQIF_PT_PROF=1
-__device__ unsigned long long g_aqif2_prof[8];
 #ifdef PAQIF_DEV_PROF
 #define AQ2_T(v) const long long v = clock64()
 #else

@@ -55,7 +55,7 @@ linesys_kernel(paqif_ehl_linesys a, int jac0, int solve, double* bands, double* 
   const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
   double* php = lsm;
   double* phm = php + N;
-  double* band = phm + N + (N & 1);  // 16-byte aligned
+  double* band = phm + N;  // 2N doubles in: 16-byte aligned
   double* rhs = band + aqif2_band_doubles(n_sys);
   double* rec = rhs + aqif2_rhs_doubles(n_sys);
   line_faces(a.q, n, a.limiter, a.kappa, php, phm, red);

@@ -889,8 +889,9 @@ extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
     unsigned long long ap[8];
     cudaMemcpyFromSymbol(ap, g_aqif2_prof, sizeof(ap));
     const double na = ap[4] ? (double)ap[4] : 1.0;
-    fprintf(stderr, "[pt_prof] aqif2 solves %llu: factor %.0f breakdown %.0f z %.0f gather %.0f cycles\n",
-            ap[4], ap[0] / na, ap[1] / na, ap[2] / na, ap[3] / na);
+    fprintf(stderr, "[pt_prof] aqif2 solves %llu: factor %.0f breakdown %.0f z %.0f gather %.0f cycles"
+            "; levels %llu, with a tiny numerator %llu\n",
+            ap[4], ap[0] / na, ap[1] / na, ap[2] / na, ap[3] / na, ap[5], ap[6]);
   }
   for (void* a : h->allocs)
     if (a) cudaFree(a);
