@@ -196,22 +196,26 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
     if (o < L * N) emit(o, first + o / N, o % N, base(first + o / N, o % N));
     return;
   }
+  bool cross = false;
+  for (int p = 0; p < count; ++p) cross |= d.meta[kMAxis + p] != mode;
+  if (nseg > 0 && !cross) {
+    // the parts of pt_films_part_kernel: one thread per output sums them in a
+    // fixed order (coalesced reads) and evaluates the rheology
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= L * N) return;
+    const int l = o / N, idx = o % N;
+    const double* src = d.fpart + (size_t)l * N + idx;
+    double v = 0.0;
+    for (int q = 0; q < count * nseg; ++q) v += src[(size_t)q * 4 * N];
+    emit(o, first + l, idx, base(first + l, idx) + v);
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const int o = blockIdx.x * kPtFilmWarps + (threadIdx.x >> 5);
   if (o >= L * N) return;
   const int l = o / N, idx = o % N;
   const int line = first + l;
   double corr = 0.0;
-  bool cross = false;
-  for (int p = 0; p < count; ++p) cross |= d.meta[kMAxis + p] != mode;
-  if (nseg > 0 && !cross) {  // parts of pt_films_part_kernel, fixed-order sum
-    double v = 0.0;
-    for (int q = lane; q < count * nseg; q += 32) v += d.fpart[((size_t)q * 4 + l) * N + idx];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) emit(o, line, idx, base(line, idx) + v);
-    return;
-  }
   for (int p = 0; p < count; ++p) {
     const int axis = d.meta[kMAxis + p], ell = d.meta[kMIdx + p];
     const double* __restrict__ delta = d.pend + (size_t)p * N;
