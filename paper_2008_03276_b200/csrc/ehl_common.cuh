@@ -154,103 +154,102 @@ __device__ __forceinline__ void line_row_entries(double rw, double rc, double re
 }
 
 // The mirrored line kernel ext[k] = table[|k - n|] (k = 0..2n; zero on 8
-// guard entries each side) in a 4-phase shared-memory layout,
-//   ext[k] at ext4[((k + 8) & 3) * Q + ((k + 8) >> 2)],  Q = ext4_q(n),
-// so that threads holding 4 consecutive outputs each read consecutive words
+// guard entries each side) in an 8-phase shared-memory layout,
+//   ext[k] at ext4[((k + 8) & 7) * Q + ((k + 8) >> 3)],  Q = ext4_q(n),
+// so that threads holding 8 consecutive outputs each read consecutive words
 // at every step of the convolution (no bank conflicts).
-__host__ __device__ inline int ext4_q(int n) { return (2 * n + 17 + 3) / 4; }
-__host__ __device__ inline int ext4_doubles(int n) { return 4 * ext4_q(n); }
+__host__ __device__ inline int ext4_q(int n) { return (2 * n + 17 + 7) / 8; }
+__host__ __device__ inline int ext4_doubles(int n) { return 8 * ext4_q(n); }
 __device__ __forceinline__ void ext4_build(const double* __restrict__ table, int n, double* ext4) {
   const int Q = ext4_q(n);
-  for (int idx = threadIdx.x; idx < 4 * Q; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < 8 * Q; idx += blockDim.x) {
     const int ph = idx / Q, q = idx - ph * Q;
-    const int k = 4 * q + ph - 8;
+    const int k = 8 * q + ph - 8;
     ext4[idx] = (k >= 0 && k <= 2 * n) ? table[k >= n ? k - n : n - k] : 0.0;
   }
 }
 __device__ __forceinline__ double ext4_at(const double* ext4, int Q, int k) {
   const int kk = k + 8;
-  return ext4[(kk & 3) * Q + (kk >> 2)];
+  return ext4[(kk & 7) * Q + (kk >> 3)];
 }
 
 // deformation: def[i] = sign * sum_j u[j] * ext[n + i - j], i = 0..n
-// (np.convolve(u, ext)[n:2n+1]), ext in the ext4 layout.  4 consecutive
-// outputs per thread sliding along the kernel: per 4 steps of j four
-// conflict-free kernel loads, four broadcast u loads, 16 DFMA.  When the
-// 4-output groups fill at most half the block, the j range is split in two
-// halves (the second added in a fixed order after a barrier); the N mod 4
+// (np.convolve(u, ext)[n:2n+1]), ext in the 8-phase layout.  8 consecutive
+// outputs per thread sliding along the kernel: per 8 steps of j eight
+// conflict-free kernel loads, eight broadcast u loads, 64 DFMA.  The j range
+// is split into S segments so that the 8-output groups fill the block; the
+// segments are added in a fixed order (one barrier each).  The N mod 8
 // outputs past the last full group are warp dot products.  All threads of
 // the CTA call.
 static __device__ void toeplitz_conv(const double* su, const double* ext4, int n, double sign,
                                      double* out) {
   const int N = n + 1, T = blockDim.x, Q = ext4_q(n);
-  const int G = N / 4;
-  const bool split = 2 * G <= T;
-  const int jh = split ? (N + 1) / 2 : N;
-  auto group = [&](int g, int j0, int j1) {
-    const int i0 = 4 * g;
-    // e_r = ext[n + i0 + r - j]; the entry entering at step j is
+  const int G = N / 8;
+  int S = G > 0 ? T / G : 1;
+  if (S < 1) S = 1;
+  if (S > 8) S = 8;
+  const int seg_len = (N + S - 1) / S;
+  auto group = [&](int g, int j0, int j1, double* a) {
+    const int i0 = 8 * g;
+    // e[r] = ext[n + i0 + r - j]; the entry entering at step j is
     // ext[n - 1 - j + i0]
-    double e0 = ext4_at(ext4, Q, n + i0 - j0), e1 = ext4_at(ext4, Q, n + i0 + 1 - j0);
-    double e2 = ext4_at(ext4, Q, n + i0 + 2 - j0), e3 = ext4_at(ext4, Q, n + i0 + 3 - j0);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double e[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      e[r] = ext4_at(ext4, Q, n + i0 + r - j0);
+      a[r] = 0.0;
+    }
     auto step = [&](double uj, double enew) {
-      a0 = fma(uj, e0, a0);
-      a1 = fma(uj, e1, a1);
-      a2 = fma(uj, e2, a2);
-      a3 = fma(uj, e3, a3);
-      e3 = e2;
-      e2 = e1;
-      e1 = e0;
-      e0 = enew;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[r] = fma(uj, e[r], a[r]);
+#pragma unroll
+      for (int r = 7; r > 0; --r) e[r] = e[r - 1];
+      e[0] = enew;
     };
     int j = j0;
-    for (; j < j1 && ((n + 7 - j) & 3) != 3; ++j) step(su[j], ext4_at(ext4, Q, n - 1 - j + i0));
-    // blocks of 4 steps: entering entries of phases 3, 2, 1, 0 at q0, then q0 - 1 ...
-    const double* p = ext4 + ((n + 7 - j) >> 2) + g;
-    for (; j + 4 <= j1; j += 4, --p) {
-      const double u0 = su[j], u1 = su[j + 1], u2 = su[j + 2], u3 = su[j + 3];
-      const double f3 = p[3 * Q], f2 = p[2 * Q], f1 = p[Q], f0 = p[0];
-      step(u0, f3);
-      step(u1, f2);
-      step(u2, f1);
-      step(u3, f0);
+    for (; j < j1 && ((n + 7 - j) & 7) != 7; ++j) step(su[j], ext4_at(ext4, Q, n - 1 - j + i0));
+    // blocks of 8 steps: entering entries of phases 7..0 at q0, then q0 - 1 ...
+    const double* p = ext4 + ((n + 7 - j) >> 3) + g;
+    for (; j + 8 <= j1; j += 8, --p) {
+      double f[8], uu[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        f[t] = p[(7 - t) * Q];
+        uu[t] = su[j + t];
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) step(uu[t], f[t]);
     }
     for (; j < j1; ++j) step(su[j], ext4_at(ext4, Q, n - 1 - j + i0));
-    return make_double4(a0, a1, a2, a3);
   };
-  if (split) {
-    const int t = threadIdx.x;
-    double4 a = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (t < G) {
-      a = group(t, 0, jh);
-      out[4 * t] = a.x;
-      out[4 * t + 1] = a.y;
-      out[4 * t + 2] = a.z;
-      out[4 * t + 3] = a.w;
-    } else if (t < 2 * G) {
-      a = group(t - G, jh, N);
+  const int t = threadIdx.x;
+  const int g = G > 0 ? t % G : 0, sg = G > 0 ? t / G : S;
+  double a[8];
+  const bool mine = sg < S && g < G;
+  if (mine) {
+    const int j0 = sg * seg_len, j1 = j0 + seg_len < N ? j0 + seg_len : N;
+    group(g, j0, j1, a);
+  }
+  for (int q = 0; q < S; ++q) {  // fixed order: segment 0, 1, ...
+    if (mine && sg == q)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double v = q == 0 ? a[r] : out[8 * g + r] + a[r];
+        out[8 * g + r] = q == S - 1 ? sign * v : v;
+      }
+    __syncthreads();
+  }
+  if (G > T) {  // more groups than threads (very long lines): remaining groups
+    for (int g2 = T + t; g2 < G; g2 += T) {
+      double b[8];
+      group(g2, 0, N, b);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) out[8 * g2 + r] = sign * b[r];
     }
     __syncthreads();
-    if (t >= G && t < 2 * G) {
-      const int i0 = 4 * (t - G);
-      out[i0] = sign * (out[i0] + a.x);
-      out[i0 + 1] = sign * (out[i0 + 1] + a.y);
-      out[i0 + 2] = sign * (out[i0 + 2] + a.z);
-      out[i0 + 3] = sign * (out[i0 + 3] + a.w);
-    }
-  } else {
-    for (int g = threadIdx.x; g < G; g += T) {
-      const double4 a = group(g, 0, N);
-      out[4 * g] = sign * a.x;
-      out[4 * g + 1] = sign * a.y;
-      out[4 * g + 2] = sign * a.z;
-      out[4 * g + 3] = sign * a.w;
-    }
   }
-  // tail outputs 4G .. N-1: one warp each, lanes striding j, fixed tree
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = 4 * G + warp; i < N; i += T >> 5) {
+  for (int i = 8 * G + warp; i < N; i += T >> 5) {
     double acc = 0.0;
     for (int j = lane; j < N; j += 32) acc = fma(su[j], ext4_at(ext4, Q, n + i - j), acc);
 #pragma unroll
