@@ -200,3 +200,29 @@ def test_device_driver_batch_stops_per_case():
     assert np.array_equal(b.u[1].cpu().numpy(), ref.u[0].cpu().numpy())
     assert list(b.hist_res[0, :5].cpu().numpy()) == res[:5]
     assert list(b.hist_res[1, :9].cpu().numpy()) == res
+
+
+def test_queued_batch_matches_one_case_launches():
+    """B > SM count: one CTA per SM pulls the cases from a queue ordered by
+    the previous step's ladder use; every case's state equals a B = 1 run of
+    the same case (bit for bit, over several steps so the order is live)."""
+    from paper_2008_03276_b200.ehl import EhlParams, LineContactBatch, moes_convert
+    rng = np.random.default_rng(11)
+    cases = list(zip(np.exp(rng.uniform(np.log(5), np.log(200), 300)), rng.uniform(5, 15, 300)))
+
+    def params(m, l):
+        u_, w_ = moes_convert(m=float(m), l=float(l), g=5000.0)
+        return EhlParams.line_from_loads(5000.0, u_, w_, domain=(-4.5, 1.5))
+
+    ps = [params(m, l) for m, l in cases]
+    b = LineContactBatch(ps, 128)
+    for _ in range(4):
+        b.step()
+    u, h0, film, res, _, info = b.snapshot()
+    for j in (0, 17, 149, 150, 299):
+        one = LineContactBatch([ps[j]], 128)
+        for _ in range(4):
+            one.step()
+        u1, h01, film1, res1, _, info1 = one.snapshot()
+        assert np.array_equal(u[j], u1[0]) and h0[j] == h01[0]
+        assert np.array_equal(film[j], film1[0]) and res[j] == res1[0] and info[j] == info1[0]
