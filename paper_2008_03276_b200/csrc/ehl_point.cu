@@ -558,12 +558,19 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
   // the rheology of the bundle's L columns came with the films
   const double* EC = d.rcache;          // [l][m] eps
   const double* RC = d.rcache + 4 * N;  // [l][m] rho
+#ifdef PAQIF_DEV_PROF
+  const long long y0 = clock64();
+  long long y1 = 0, y2 = 0, y3 = 0;
+#endif
   double qmax = 0.0;
   for (int k = threadIdx.x; k < L * N; k += blockDim.x) {
     const int l = k / N, m = k % N;
     qmax = fmax(qmax, fabs(RC[k] * film(l, m)));
   }
   const double gfloor = 1e-12 * fmax(block_max(qmax, S.red), kRatioGuard);
+#ifdef PAQIF_DEV_PROF
+  y1 = clock64();
+#endif
   const double* t = d.table;
   const double s00 = t[0], s10 = t[N], s01 = t[1], s11 = t[N + 1];
   double* band = sysb;
@@ -626,7 +633,13 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
       put_row1(band, rhs, n_sys, n_int, r, e, rr);
     }
     if (rung == 0) note_worst(d, worst, S.red);
+#ifdef PAQIF_DEV_PROF
+    if (rung == 0) y2 = clock64();
+#endif
     st = aqif1_solve<EXACT>(band, rhs, n_sys, rec, band, &S.flag) & 1;
+#ifdef PAQIF_DEV_PROF
+    if (rung == 0) y3 = clock64();
+#endif
     if (!st) break;
   }
   if (st) {
@@ -667,6 +680,11 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
       if (p + 1 > 8) d.meta[kMGate] = 1;
     }
   }
+#ifdef PAQIF_DEV_PROF
+  if (threadIdx.x == 0 && i == d.n / 2)
+    printf("[y_prof] n=%d pass1 %lld assemble %lld solve %lld update %lld\n", d.n, y1 - y0,
+           y2 - y1, y3 - y2, clock64() - y3);
+#endif
 }
 
 // force balance (sweeps.py:521-535, weight h^2)
