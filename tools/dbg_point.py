@@ -1,3 +1,4 @@
+"""Dev: point-contact debugging helper (one step, dumps of device state)."""
 import sys, time, numpy as np
 sys.path.insert(0, '/root/repo')
 from paper_2008_03276_b200.ehl import EhlParams, PointContact

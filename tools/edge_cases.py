@@ -1,3 +1,4 @@
+"""Dev: point / line drivers at edge-case grid sizes (8 .. 4096 intervals)."""
 import sys; sys.path.insert(0, "/root/repo")
 import numpy as np
 from paper_2008_03276_b200.ehl import EhlParams, PointContact, LineContactBatch, moes_convert, solve_ehl

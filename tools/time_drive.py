@@ -1,3 +1,4 @@
+"""Dev: solve_ehl with device-side stop tests vs the per-iteration host loop."""
 import time, sys
 sys.path.insert(0, "/root/repo")
 from paper_2008_03276_b200.ehl import solve_ehl, EhlParams, moes_convert

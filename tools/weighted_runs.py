@@ -1,3 +1,4 @@
+"""Dev: runs of deferred (weighted) x-lines per outer iteration and their stability."""
 import sys
 sys.path.insert(0, "/root/repo")
 import numpy as np

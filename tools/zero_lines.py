@@ -1,3 +1,4 @@
+"""Dev: rows / columns of the point contact that stay all-zero or unchanged per step."""
 import sys
 sys.path.insert(0, "/root/repo")
 import numpy as np
