@@ -234,6 +234,16 @@ int paqif_ehl_point_film_lines(paqif_ehl_point *h, int32_t mode, const int32_t *
 /* Deformation of HOST pressure u into HOST out (FilmModel.deformation_full). */
 int paqif_ehl_point_deformation(paqif_ehl_point *h, const double *u, double *out);
 
+/* Deformation kernel tables on the device (ehl/kernels.py:64-100,
+ * kernel_line / kernel_point): table [dev] nx+1 doubles, the cell integrals
+ * of log|x - x'| for offsets 0..nx; or (nx+1) x (ny+1) row-major, the
+ * eight-term asinh form times `scale` (the caller passes 2.0 / np.pi**2 so
+ * the constant is the reference's).  Within a few ulp of the host tables
+ * (library log / asinh rounding). */
+int paqif_ehl_kernel_line(int64_t nx, double h, double *table, void *stream);
+int paqif_ehl_kernel_point(int64_t nx, int64_t ny, double h, double scale, double *table,
+                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

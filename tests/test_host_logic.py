@@ -146,6 +146,18 @@ class TestEhlHost:
         assert load_kernel_cache(path, "point", 0.2, 8, 8) is None
         assert load_kernel_cache(path, "line", 0.1, 8) is None
 
+    def test_kernel_tables_vs_reference(self):
+        # host tables bit-identical to the reference's (golden ehl_kernels.npz)
+        from conftest import load_golden
+        from paper_2008_03276_b200.ehl import kernel_line, kernel_point
+        K = load_golden("ehl_kernels.npz")
+        for k in (0, 1):
+            t = kernel_line(int(K[f"line{k}_n"]), float(K[f"line{k}_h"])).table
+            assert np.array_equal(t, K[f"line{k}_table"])
+            t = kernel_point(int(K[f"point{k}_nx"]), int(K[f"point{k}_ny"]),
+                             float(K[f"point{k}_h"])).table
+            assert np.array_equal(t, K[f"point{k}_table"])
+
     def test_params(self):
         from paper_2008_03276_b200.ehl import EhlParams, moes_convert, moes_from_line
         u, w = moes_convert(m=20.0, l=10.0, g=5000.0)
