@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"] + ARCH
 
 SOURCES = ["dropin.cu", "lcp.cu", "version.cu", "ehl_line.cu", "ehl_point.cu", "rblock.cu",
-           "ehl_linesys.cu", "ehl_kernels.cu"]
+           "ehl_linesys.cu", "ehl_kernels.cu", "tvd_sweep.cu"]
 
 
 def _nvcc() -> str:

@@ -226,3 +226,42 @@ def test_weak_scaling_shards_gloo():
     got_u = np.concatenate([g[0] for g in gathered])
     got_p = np.concatenate([g[1] for g in gathered])
     assert np.array_equal(got_u, u) and np.array_equal(got_p, passes)
+
+
+class TestTvdHost:
+    """Host set-up of the TVD study (tvdcd.py mirror): the operator and
+    residual norm reproduce the reference's residual norms bit for bit
+    (golden tvd.npz), plus the contract errors and study helpers."""
+
+    def test_residual_norm_vs_reference(self):
+        from conftest import load_golden
+        from paper_2008_03276_b200.tvdcd import (ConvectionDiffusionProblem, Grid2D,
+                                                 KappaSchemeConfig)
+        T = load_golden("tvd.npz")
+        prob = ConvectionDiffusionProblem(Grid2D(0.0, 1.0, 0.0, 1.0, 19, 19),
+                                          KappaSchemeConfig(kappa=0.0, eps=1e-4, a=1.0, b=0.7),
+                                          T["c_upwind_ls0__f"], T["c_upwind_ls0__boundary"],
+                                          closure="upwind")
+        assert prob.residual_norm(T["c_upwind_ls0__u1"]) == T["c_upwind_ls0__res"][0]
+        assert prob.residual_norm(T["c_upwind_ls0__u2"]) == T["c_upwind_ls0__res"][1]
+
+    def test_contracts_and_helpers(self):
+        from paper_2008_03276_b200.tvdcd import (Grid2D, KappaSchemeConfig, convergence_order,
+                                                 error_norms, transposed_problem,
+                                                 quartic_test_problem)
+        g = Grid2D.square(16)
+        assert g.h == pytest.approx(2.0 / 16) and g.nx == 15
+        with pytest.raises(ContractViolationError):
+            Grid2D(0.0, 1.0, 0.0, 2.0, 7, 7)
+        with pytest.raises(ContractViolationError):
+            KappaSchemeConfig(kappa=1.5)
+        with pytest.raises(ContractViolationError):
+            quartic_test_problem(4, KappaSchemeConfig())
+        u = np.ones((4, 4))
+        assert error_norms(u, u, 0.1) == (0.0, 0.0, 0.0)
+        assert convergence_order([1.0, 0.5, 0.25]) == pytest.approx([1.0, 1.0])
+        prob, exact = quartic_test_problem(16, KappaSchemeConfig(kappa=1 / 3, eps=1e-6))
+        twin = transposed_problem(prob)
+        r1 = prob.residual_field(exact)
+        r2 = twin.residual_field(np.ascontiguousarray(exact.T))
+        assert np.allclose(r1, r2.T, atol=1e-12)
