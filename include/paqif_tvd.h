@@ -29,6 +29,14 @@ typedef struct {
   const double *cx;      /* [dev] kx planes */
   const double *cy;      /* [dev] ky planes */
   const double *lb;      /* [dev] 4 planes: line bands at offsets -2..+1 */
+  /* Shared line factorization (constant-coefficient lines, as the
+   * reference caches it, tvdcd.py:466-477): the WZFactors arrays of
+   * paqif_factor_batch for one system of the padded line order, [dev];
+   * z2x2 NULL = factor every line.  Then each line is solve_w + solve_z
+   * (aqif.py:138-178) on the shared factors. */
+  const double *z2x2, *zl, *zr, *ww;
+  int32_t zf_beta;
+  int32_t reserved2;
 } paqif_tvd_problem;
 
 /* sweep_splitting(problem, u, variant in {Ls0, Ls1, Ls2}, omega, order)

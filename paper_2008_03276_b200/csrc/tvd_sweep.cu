@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "aqif2.cuh"
 #include "capi_util.cuh"
@@ -100,6 +101,104 @@ __device__ double pairwise_sum(const double* a, int64_t n) {
   return ret;
 }
 
+// solve_w + solve_z of one line on shared WZ factors (aqif.py:138-178,
+// _kernels.py:152-225), reference operation order; one thread, y and x in
+// shared memory.  Returns 0 or the 1-based Z breakdown level.
+struct SharedFactors {
+  const double *z2x2, *zl, *zr, *ww;
+  const double *det, *rcp;  // per level: the 2x2 determinant, RN(1/det)
+  const int* fl;            // per level: bit 0 det in the Markstein range, bit 1 breakdown
+};
+
+// The W and Z chains keep the unknowns they are about to reuse in
+// registers (a window of BETA values per side that slides one row per
+// level), so a level waits on its own arithmetic, not on shared memory.
+template <int BETA>
+__device__ int shared_line_solve(const SharedFactors& p, int n, double* __restrict__ y,
+                                 double* __restrict__ x) {
+  using A = Arith<true>;
+  constexpr int TB = 2 * BETA, BP1 = BETA + 1;
+  const int s = n / 2;
+  const double* __restrict__ ww = p.ww;
+  const double* __restrict__ zl = p.zl;
+  const double* __restrict__ zr = p.zr;
+  const double* __restrict__ z2 = p.z2x2;
+  // W0 y = r, middle-out (solve_w_batch): wt[t] = y[rt - BETA + t],
+  // wb[t] = y[rb + 1 + t] of the current level
+  double wt[BETA], wb[BETA];
+  double cur_t = y[s - 1], cur_b = y[s];
+#pragma unroll
+  for (int t = 0; t < BETA; ++t) {
+    const int it = s - 1 - BETA + t, ib = s + 1 + t;
+    wt[t] = it >= 0 ? y[it] : 0.0;
+    wb[t] = ib < n ? y[ib] : 0.0;
+  }
+  for (int k = 1; k <= s; ++k) {
+    const int rt = s - k, rb = s + k - 1;
+    const double yt = cur_t, yb = cur_b;
+    const double* wk = ww + (size_t)k * TB * 2;
+#pragma unroll
+    for (int t = 0; t < BETA; ++t) {
+      if (rt - BETA + t >= 0)
+        wt[t] = A::sub(wt[t], A::add(A::mul(yt, wk[t * 2]), A::mul(yb, wk[t * 2 + 1])));
+      if (rb + 1 + t < n)
+        wb[t] = A::sub(wb[t], A::add(A::mul(yt, wk[(BETA + t) * 2]),
+                                     A::mul(yb, wk[(BETA + t) * 2 + 1])));
+    }
+    y[rt] = yt;  // final: no later level touches rows rt, rb
+    y[rb] = yb;
+    cur_t = wt[BETA - 1];
+    cur_b = wb[0];
+#pragma unroll
+    for (int t = BETA - 1; t > 0; --t) wt[t] = wt[t - 1];
+#pragma unroll
+    for (int t = 0; t < BETA - 1; ++t) wb[t] = wb[t + 1];
+    const int it = rt - 1 - BETA, ib = rb + 1 + BETA;
+    wt[0] = it >= 0 ? y[it] : 0.0;
+    wb[BETA - 1] = ib < n ? y[ib] : 0.0;
+  }
+  // Z0 x = y, outside-in (solve_z_batch, start level 1): xl[t] =
+  // x[pp - BETA + t], xr[t] = x[q + 1 + t]
+  double xl[BETA], xr[BETA];
+#pragma unroll
+  for (int t = 0; t < BETA; ++t) xl[t] = xr[t] = 0.0;
+  for (int level = 1; level <= s; ++level) {
+    const int pp = level - 1, q = n - 1 - pp, k = s - pp;
+    const double* zlk = zl + (size_t)k * 2 * BP1;
+    const double* zrk = zr + (size_t)k * 2 * BP1;
+    double rt_rhs = y[pp], rb_rhs = y[q];
+#pragma unroll
+    for (int t = 0; t < BETA; ++t) {
+      if (pp - BETA + t >= 0) {
+        rt_rhs = A::axpy_neg(rt_rhs, zlk[t], xl[t]);
+        rb_rhs = A::axpy_neg(rb_rhs, zlk[BP1 + t], xl[t]);
+      }
+      if (q + 1 + t < n) {
+        rt_rhs = A::axpy_neg(rt_rhs, zrk[1 + t], xr[t]);
+        rb_rhs = A::axpy_neg(rb_rhs, zrk[BP1 + 1 + t], xr[t]);
+      }
+    }
+    const double* zk = z2 + (size_t)k * 4;
+    const double a11 = zk[0], a12 = zk[1], a21 = zk[2], a22 = zk[3];
+    const double det = p.det[k], yr = p.rcp[k];
+    const int fl = p.fl[k];
+    if (fl & 2) return level;
+    const bool ds = fl & 1;
+    // RN quotient through the reciprocal (Markstein), __ddiv_rn out of range
+    const double xp = div_rn(A::det2(a22, rt_rhs, a12, rb_rhs), det, yr, ds);
+    const double xq = div_rn(A::det2(a11, rb_rhs, a21, rt_rhs), det, yr, ds);
+    x[pp] = xp;
+    x[q] = xq;
+#pragma unroll
+    for (int t = 0; t < BETA - 1; ++t) xl[t] = xl[t + 1];
+    xl[BETA - 1] = xp;
+#pragma unroll
+    for (int t = BETA - 1; t > 0; --t) xr[t] = xr[t - 1];
+    xr[0] = xq;
+  }
+  return 0;
+}
+
 __global__ void __launch_bounds__(kTvdThreads, 1)
 tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, double* resid,
                  double* norm, int32_t* status) {
@@ -111,36 +210,93 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
   double* rhs = band + aqif2_band_doubles(n);
   double* rec = rhs + aqif2_rhs_doubles(n);
   const size_t plane = (size_t)nx * ny;
-  aqif2_zero_pads(band, rhs, n);
+  if (!p.z2x2) aqif2_zero_pads(band, rhs, n);
+  // shared factors staged in shared memory once: the line solves' chains
+  // then wait on shared-memory, not L2, latency
+  SharedFactors fz{};
+  if (p.z2x2) {
+    const int s = n / 2, bp1 = p.zf_beta + 1, tb = 2 * p.zf_beta;
+    double* d = rec + (size_t)(n / 2 + 1) * kRec2;
+    const size_t c4 = (size_t)(s + 1) * 4, cz = (size_t)(s + 1) * 2 * bp1,
+                 cw = (size_t)(s + 1) * 2 * tb;
+    for (size_t i = threadIdx.x; i < c4; i += blockDim.x) d[i] = p.z2x2[i];
+    for (size_t i = threadIdx.x; i < cz; i += blockDim.x) d[c4 + i] = p.zl[i];
+    for (size_t i = threadIdx.x; i < cz; i += blockDim.x) d[c4 + cz + i] = p.zr[i];
+    for (size_t i = threadIdx.x; i < cw; i += blockDim.x) d[c4 + 2 * cz + i] = p.ww[i];
+    double* dd = d + c4 + 2 * cz + cw;
+    double* rr = dd + (s + 1);
+    int* fl = reinterpret_cast<int*>(rr + (s + 1));
+    __syncthreads();
+    // the level's 2x2 pivot test and reciprocal depend on the factors only
+    // (solve_z_batch, _kernels.py:175-225): once per sweep
+    for (int k = 1 + threadIdx.x; k <= s; k += blockDim.x) {
+      using A = Arith<true>;
+      const double* zk = d + (size_t)k * 4;
+      const double a11 = zk[0], a12 = zk[1], a21 = zk[2], a22 = zk[3];
+      const double det = A::det2(a11, a22, a12, a21);
+      double scale = fabs(a11);
+      if (fabs(a12) > scale) scale = fabs(a12);
+      if (fabs(a21) > scale) scale = fabs(a21);
+      if (fabs(a22) > scale) scale = fabs(a22);
+      const bool bad = fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY;
+      dd[k] = det;
+      rr[k] = __drcp_rn(det);
+      fl[k] = (div_safe(det) ? 1 : 0) | (bad ? 2 : 0);
+    }
+    fz = SharedFactors{d, d + c4, d + c4 + cz, d + c4 + 2 * cz, dd, rr, fl};
+    __syncthreads();
+  }
   int st = 0;
   for (int jj = 0; jj < ny; ++jj) {
     const int j = backward ? ny - 1 - jj : jj;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) {
-      // _line_matrix: identity diagonal, then the line's bands on rows
-      // r < nx (columns may reach the pinned pad unknowns), out-of-range
-      // columns zero
-      double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
-      double rr = 0.0;
-      if (r < nx) {
-        const size_t k = (size_t)j * nx + r;
-        for (int t = 0; t < 4; ++t) {
-          const int o = t - 2;  // line band offsets -2, -1, 0, +1
-          if (!(p.line_mask & (1 << t)) || r + o < 0) continue;
-          e[o + 2] = p.lb[t * plane + k];
+    if (p.z2x2) {
+      // shared factors: the line's residual is the right side of W0 Z0
+      double* y = rhs;
+      double* x = band;
+      for (int r = threadIdx.x; r < n; r += blockDim.x)
+        y[r] = r < nx ? p.f[(size_t)j * nx + r] - apply_at(p, uf, j, r) : 0.0;
+      __syncthreads();
+#ifdef PAQIF_TVD_PROF
+      const long long t0 = clock64();
+#endif
+      if (threadIdx.x == 0)
+        flag = p.zf_beta == 1 ? shared_line_solve<1>(fz, n, y, x) : shared_line_solve<2>(fz, n, y, x);
+#ifdef PAQIF_TVD_PROF
+      if (threadIdx.x == 0 && jj == ny / 2) printf("tvd line solve %lld cycles (n=%d)\n", clock64() - t0, n);
+#endif
+      __syncthreads();
+      if (flag) {
+        st = j + 1;
+        break;
+      }
+    } else {
+      for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        // _line_matrix: identity diagonal, then the line's bands on rows
+        // r < nx (columns may reach the pinned pad unknowns), out-of-range
+        // columns zero
+        double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
+        double rr = 0.0;
+        if (r < nx) {
+          const size_t k = (size_t)j * nx + r;
+          for (int t = 0; t < 4; ++t) {
+            const int o = t - 2;  // line band offsets -2, -1, 0, +1
+            if (!(p.line_mask & (1 << t)) || r + o < 0) continue;
+            e[o + 2] = p.lb[t * plane + k];
+          }
+          rr = p.f[k] - apply_at(p, uf, j, r);
         }
-        rr = p.f[k] - apply_at(p, uf, j, r);
-      }
 #pragma unroll
-      for (int d = 0; d < 5; ++d) {
-        const int col = r + d - 2;
-        band2_ref(band, n, r, d - 2) = (col >= 0 && col < n) ? e[d] : 0.0;
+        for (int d = 0; d < 5; ++d) {
+          const int col = r + d - 2;
+          band2_ref(band, n, r, d - 2) = (col >= 0 && col < n) ? e[d] : 0.0;
+        }
+        rhs[kBandPad + r] = rr;
       }
-      rhs[kBandPad + r] = rr;
-    }
-    const int s = aqif2_solve<true>(band, rhs, n, rec, band, &flag);
-    if (s & 1) {
-      st = j + 1;
-      break;
+      const int s = aqif2_solve<true>(band, rhs, n, rec, band, &flag);
+      if (s & 1) {
+        st = j + 1;
+        break;
+      }
     }
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
       double* c = uf + (size_t)(2 + j) * W + 2 + i;
@@ -175,9 +331,11 @@ __global__ void tvd_transpose_kernel(const double* src, int ny, int nx, double* 
   }
 }
 
-size_t tvd_smem(int nx) {
+size_t tvd_smem(int nx, int zf_beta) {
   const int n = (nx + 1) % 2 == 0 ? nx + 1 : nx + 2;
-  return (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) + (size_t)(n / 2 + 1) * kRec2) * 8;
+  const size_t fz =
+      zf_beta ? (size_t)(n / 2 + 1) * (4 + 4 * (zf_beta + 1) + 4 * zf_beta + 3) : 0;
+  return (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) + (size_t)(n / 2 + 1) * kRec2 + fz) * 8;
 }
 
 }  // namespace paqif
@@ -193,13 +351,14 @@ extern "C" int paqif_tvd_sweep(const paqif_tvd_problem* p, double* u_full, int32
                                void* stream) {
   if (!p || p->nx < 2 || p->ny < 1 || !p->f || !p->c0 || !p->lb || !u_full || !status ||
       p->kx < 0 || p->kx > 4 || p->ky < 0 || p->ky > 4 || (p->kx && !p->cx) ||
+      (p->z2x2 && (!p->zl || !p->zr || !p->ww || p->zf_beta < 1 || p->zf_beta > 2)) ||
       (p->ky && !p->cy) || (want_norm && (!resid || !norm)))
     return set_arg_error("paqif_tvd_sweep: problem / buffers");
   for (int t = 0; t < p->kx; ++t)
     if (p->ox[t] < -2 || p->ox[t] > 2) return set_arg_error("paqif_tvd_sweep: x offset");
   for (int t = 0; t < p->ky; ++t)
     if (p->oy[t] < -2 || p->oy[t] > 2) return set_arg_error("paqif_tvd_sweep: y offset");
-  const size_t smem = tvd_smem(p->nx);
+  const size_t smem = tvd_smem(p->nx, p->z2x2 ? p->zf_beta : 0);
   if (smem > 227 * 1024) return set_arg_error("paqif_tvd_sweep: line too long for one CTA");
   cudaFuncSetAttribute(tvd_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tvd_sweep_kernel<<<1, kTvdThreads, smem, (cudaStream_t)stream>>>(*p, u_full, backward,

@@ -9,7 +9,10 @@ the reference, and runs once per problem.  The sweeps -- the part that
 repeats -- run on the device: one CTA per sweep walks the x-lines in order
 (residual line, padded AQIF line solve, relaxed update) and ends with the
 residual norm in numpy's summation order (csrc/tvd_sweep.cu,
-include/paqif_tvd.h), bit for bit the reference's iterates.
+include/paqif_tvd.h), bit for bit the reference's iterates.  Lines with
+varying coefficients are factored one by one on the beta = 2 latency
+engine; constant-coefficient lines share one factorization, as in the
+reference, and each line is then only W and Z solves.
 
 Variants on the device: Ls0, Ls1, Ls2.  DefC (a sparse direct first-order
 solve, tvdcd.py:553-570) and Ls3 (documented as not robust,
@@ -239,6 +242,24 @@ def _line_system_coeffs(problem: ConvectionDiffusionProblem, variant: str) -> di
     return bands
 
 
+def _padded_even_order(nx: int) -> int:
+    return nx + 1 if (nx + 1) % 2 == 0 else nx + 2
+
+
+def _line_matrix(band_rows: dict, nx: int, beta: int):
+    """Line matrix padded with pinned trailing unknowns to an even order
+    (tvdcd.py:424-436)."""
+    from .bandcore import BandedMatrix
+    mat = BandedMatrix(_padded_even_order(nx), beta)
+    mat.bands[beta, :] = 1.0
+    for off, vals in band_rows.items():
+        lo = max(0, -off)
+        mat.bands[beta + off][lo:nx] = vals[lo:nx]
+    mat.bands[beta, nx:] = 1.0
+    mat._zero_out_of_range()
+    return mat
+
+
 def transposed_problem(problem: ConvectionDiffusionProblem) -> ConvectionDiffusionProblem:
     """x and y exchanged, so a y-sweep is an x-sweep of the twin
     (tvdcd.py:492-511)."""
@@ -265,7 +286,9 @@ class _TvdProblem(_ct.Structure):
                 ("line_mask", _ct.c_int32), ("reserved", _ct.c_int32),
                 ("omega", _ct.c_double), ("h2", _ct.c_double), ("f", _ct.c_void_p),
                 ("c0", _ct.c_void_p), ("cx", _ct.c_void_p), ("cy", _ct.c_void_p),
-                ("lb", _ct.c_void_p)]
+                ("lb", _ct.c_void_p), ("z2x2", _ct.c_void_p), ("zl", _ct.c_void_p),
+                ("zr", _ct.c_void_p), ("ww", _ct.c_void_p), ("zf_beta", _ct.c_int32),
+                ("reserved2", _ct.c_int32)]
 
 
 def _lib():
@@ -319,6 +342,18 @@ class _DeviceSplitting:
         s.f, s.c0, s.cx, s.cy, s.lb = (self.f.data_ptr(), self.c0.data_ptr(),
                                        self.cx.data_ptr(), self.cy.data_ptr(),
                                        self.lb.data_ptr())
+        # constant-coefficient problems share one line factorization, as
+        # the reference caches it (tvdcd.py:466-477): factored once
+        # (paqif_factor_batch), each line then only solve_w + solve_z
+        cfg = problem.cfg
+        if not (callable(cfg.a) or callable(cfg.b)) and all(
+                np.ptp(c, axis=0).max() == 0.0 for c in bands.values()):
+            from .aqif import factorize_wz
+            beta = 2 if -2 in bands else 1
+            fac = factorize_wz(_line_matrix({o: c[0] for o, c in bands.items()}, nx, beta))
+            self.fac = [dev(a) for a in (fac.z2x2, fac.zl, fac.zr, fac.ww)]
+            s.z2x2, s.zl, s.zr, s.ww = (t.data_ptr() for t in self.fac)
+            s.zf_beta = beta
         self.struct = s
         self.shape = (ny, nx)
 
