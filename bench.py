@@ -254,7 +254,30 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
     out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
     for v in out.values():
         v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
+    out["tvd"] = tvd_secondary()
     return out
+
+
+def tvd_secondary(intervals=256, sweeps=4):
+    """TVD linear study: Ls1 x-line sweeps of the
+    manufactured quartic problem (kappa = 1/3), solve_by_sweeps on the
+    device (csrc/tvd_sweep.cu), device-timed; bit-exact iterates."""
+    import torch
+    from paper_2008_03276_b200.tvdcd import KappaSchemeConfig, quartic_test_problem, solve_by_sweeps
+    prob, _ = quartic_test_problem(intervals, KappaSchemeConfig(kappa=1.0 / 3.0, eps=1e-6))
+    solve_by_sweeps(prob, "Ls1", tol=0.0, max_sweeps=1, cycle="x")
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    _, hist = solve_by_sweeps(prob, "Ls1", tol=0.0, max_sweeps=sweeps, cycle="x")
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / sweeps
+    return {"metric": "TVD Ls1 x-line sweeps/s (quartic problem, kappa=1/3)",
+            "value": 1e3 / ms, "unit": "sweeps/s", "ms_per_sweep": ms,
+            "intervals": intervals, "lines_per_sweep": prob.grid.ny,
+            "residual_last": hist[-1], "arith": "exact (reference rounding)"}
 
 
 def point_secondary(with_cpu, steps4=3, steps5=1):
