@@ -42,10 +42,31 @@ __device__ __forceinline__ double apply_at(const paqif_tvd_problem& p, const dou
   return v;
 }
 
+// (L u)[j, i] split around the term that reads row j + od (the line solved
+// just before line j): the sum of the terms before it (returned) and the
+// products after it (rest[], at most 3), so the line's right side can be
+// finished with one product once that row is updated -- same order, same
+// bits as apply_at.  dep < 0: no such term, everything summed.
+__device__ __forceinline__ double apply_split(const paqif_tvd_problem& p, const double* uf, int j,
+                                              int i, int dep, double* rest) {
+  const int W = p.nx + 4;
+  const size_t k = (size_t)j * p.nx + i;
+  const double* c = uf + (size_t)(2 + j) * W + 2 + i;
+  const size_t plane = (size_t)p.nx * p.ny;
+  double v = dmul(p.c0[k], c[0]);
+  for (int t = 0; t < p.kx; ++t) v = dadd(v, dmul(p.cx[t * plane + k], c[p.ox[t]]));
+  for (int t = 0; t < p.ky; ++t) {
+    const double term = dmul(p.cy[t * plane + k], c[(ptrdiff_t)p.oy[t] * W]);
+    if (dep < 0 || t < dep) v = dadd(v, term);
+    else if (t > dep) rest[t - dep - 1] = term;
+  }
+  return v;
+}
+
 // numpy's pairwise sum of a contiguous float64 array: leaves of <= 128
 // summed with 8 accumulators, longer runs split at half rounded down to a
-// multiple of 8 and the halves added.  One thread; the recursion is run on
-// an explicit stack (the call stack would overflow at study sizes).
+// multiple of 8 and the halves added (the recursion runs on an explicit
+// stack: the call stack would overflow at study sizes).
 __device__ double pairwise_leaf(const double* a, int64_t n) {
   if (n < 8) {
     double res = 0.0;
@@ -65,7 +86,10 @@ __device__ double pairwise_leaf(const double* a, int64_t n) {
   return res;
 }
 
-__device__ double pairwise_sum(const double* a, int64_t n) {
+// The pairwise recursion walked depth-first on an explicit stack; at each
+// leaf, LEAF(offset, length) gives its sum.
+template <typename Leaf>
+__device__ double pairwise_walk(int64_t n, Leaf leaf) {
   struct Frame {
     int64_t off, n;
     double left;
@@ -78,7 +102,7 @@ __device__ double pairwise_sum(const double* a, int64_t n) {
   while (sp >= 0) {
     Frame& f = st[sp];
     if (f.n <= 128) {
-      ret = pairwise_leaf(a + f.off, f.n);
+      ret = leaf(f.off, f.n);
       --sp;
       continue;
     }
@@ -99,6 +123,23 @@ __device__ double pairwise_sum(const double* a, int64_t n) {
     }
   }
   return ret;
+}
+
+// numpy's pairwise sum of a (global, CTA-private) array with all threads of
+// the CTA: leaf sums in parallel (thread t takes leaves t, t + blockDim,
+// ... of the depth-first order and leaves each sum in its leaf's first
+// slot), then thread 0 combines them in the recursion's order.  All
+// threads call; the result is valid on thread 0.
+__device__ double pairwise_sum_cta(double* a, int64_t n) {
+  int64_t idx = 0;
+  pairwise_walk(n, [&](int64_t off, int64_t len) {
+    if (idx++ % blockDim.x == threadIdx.x) a[off] = pairwise_leaf(a + off, len);
+    return 0.0;
+  });
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) r = pairwise_walk(n, [&](int64_t off, int64_t) { return a[off]; });
+  return r;
 }
 
 // solve_w + solve_z of one line on shared WZ factors (aqif.py:138-178,
@@ -247,29 +288,66 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
     __syncthreads();
   }
   int st = 0;
-  for (int jj = 0; jj < ny; ++jj) {
-    const int j = backward ? ny - 1 - jj : jj;
-    if (p.z2x2) {
-      // shared factors: the line's residual is the right side of W0 Z0
-      double* y = rhs;
-      double* x = band;
-      for (int r = threadIdx.x; r < n; r += blockDim.x)
-        y[r] = r < nx ? p.f[(size_t)j * nx + r] - apply_at(p, uf, j, r) : 0.0;
-      __syncthreads();
-#ifdef PAQIF_TVD_PROF
-      const long long t0 = clock64();
-#endif
-      if (threadIdx.x == 0)
-        flag = p.zf_beta == 1 ? shared_line_solve<1>(fz, n, y, x) : shared_line_solve<2>(fz, n, y, x);
-#ifdef PAQIF_TVD_PROF
-      if (threadIdx.x == 0 && jj == ny / 2) printf("tvd line solve %lld cycles (n=%d)\n", clock64() - t0, n);
-#endif
+  if (p.z2x2) {
+    // shared factors: warp 0 runs the line's W + Z chain while the other
+    // warps form the next line's right side up to the term that reads the
+    // row being solved; after the solve each thread updates its column of
+    // that row and finishes the next right side with one product
+    double* y = rhs;
+    double* x = band;
+    double* part = const_cast<double*>(fz.rcp) + (n / 2 + 1) + (n / 2 + 2) / 2;  // after the flags
+    double* rest = part + nx;                              // 3 planes of nx
+    const int od = backward ? 1 : -1;
+    int dep = -1;
+    for (int t = 0; t < p.ky; ++t)
+      if (p.oy[t] == od && dep < 0) dep = t;
+    const int j0 = backward ? ny - 1 : 0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x)
+      y[r] = r < nx ? p.f[(size_t)j0 * nx + r] - apply_at(p, uf, j0, r) : 0.0;
+    __syncthreads();
+    for (int jj = 0; jj < ny; ++jj) {
+      const int j = backward ? ny - 1 - jj : jj;
+      const int jn = jj + 1 < ny ? (backward ? j - 1 : j + 1) : -1;
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+          flag = p.zf_beta == 1 ? shared_line_solve<1>(fz, n, y, x)
+                                : shared_line_solve<2>(fz, n, y, x);
+      } else if (jn >= 0) {
+        for (int i = threadIdx.x - 32; i < nx; i += blockDim.x - 32) {
+          double r3[3];
+          part[i] = apply_split(p, uf, jn, i, dep, r3);
+          for (int t = 0; dep >= 0 && t < p.ky - dep - 1; ++t) rest[t * nx + i] = r3[t];
+        }
+      }
       __syncthreads();
       if (flag) {
         st = j + 1;
         break;
       }
-    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i >= nx) {
+          y[i] = 0.0;  // pinned pad unknowns (the W sweep wrote them)
+          continue;
+        }
+        double* c = uf + (size_t)(2 + j) * W + 2 + i;
+        const double un = dadd(*c, dmul(p.omega, x[i]));
+        *c = un;
+        if (jn >= 0) {
+          const size_t k = (size_t)jn * nx + i;
+          double v = part[i];
+          if (dep >= 0) {
+            v = dadd(v, dmul(p.cy[dep * plane + k], un));
+            for (int t = 0; t < p.ky - dep - 1; ++t) v = dadd(v, rest[t * nx + i]);
+          }
+          y[i] = p.f[k] - v;
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+  for (int jj = 0; jj < ny; ++jj) {
+    const int j = backward ? ny - 1 - jj : jj;
+    {
       for (int r = threadIdx.x; r < n; r += blockDim.x) {
         // _line_matrix: identity diagonal, then the line's bands on rows
         // r < nx (columns may reach the pinned pad unknowns), out-of-range
@@ -304,6 +382,7 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
     }
     __syncthreads();
   }
+  }
   if (threadIdx.x == 0) *status = st;
   if (!want_norm || st) return;
   for (int64_t k = threadIdx.x; k < (int64_t)plane; k += blockDim.x) {
@@ -312,7 +391,8 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
     resid[k] = dmul(r, r);
   }
   __syncthreads();
-  if (threadIdx.x == 0) *norm = sqrt(dmul(p.h2, pairwise_sum(resid, (int64_t)plane)));
+  const double sum = pairwise_sum_cta(resid, (int64_t)plane);
+  if (threadIdx.x == 0) *norm = sqrt(dmul(p.h2, sum));
 }
 
 // interior of a (ny+4) x (nx+4) field into the interior of the transposed
@@ -334,7 +414,8 @@ __global__ void tvd_transpose_kernel(const double* src, int ny, int nx, double* 
 size_t tvd_smem(int nx, int zf_beta) {
   const int n = (nx + 1) % 2 == 0 ? nx + 1 : nx + 2;
   const size_t fz =
-      zf_beta ? (size_t)(n / 2 + 1) * (4 + 4 * (zf_beta + 1) + 4 * zf_beta + 3) : 0;
+      zf_beta ? (size_t)(n / 2 + 1) * (4 + 4 * (zf_beta + 1) + 4 * zf_beta + 3) + 4 * (size_t)nx + 8
+              : 0;
   return (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) + (size_t)(n / 2 + 1) * kRec2 + fz) * 8;
 }
 
