@@ -309,9 +309,16 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
       const int j = backward ? ny - 1 - jj : jj;
       const int jn = jj + 1 < ny ? (backward ? j - 1 : j + 1) : -1;
       if (threadIdx.x < 32) {
-        if (threadIdx.x == 0)
+        if (threadIdx.x == 0) {
+#ifdef PAQIF_TVD_PROF
+          const long long t0 = clock64();
+#endif
           flag = p.zf_beta == 1 ? shared_line_solve<1>(fz, n, y, x)
                                 : shared_line_solve<2>(fz, n, y, x);
+#ifdef PAQIF_TVD_PROF
+          if (jj == ny / 2) printf("tvd W+Z line solve %lld cycles (n=%d)\n", clock64() - t0, n);
+#endif
+        }
       } else if (jn >= 0) {
         for (int i = threadIdx.x - 32; i < nx; i += blockDim.x - 32) {
           double r3[3];
