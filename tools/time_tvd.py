@@ -21,3 +21,16 @@ for iv in (64, 128, 256, 512):
     dt = (time.perf_counter() - t) / k
     print(f"{'ref' if ref else 'gpu'} intervals={iv} lines={prob.grid.ny} ms/sweep={dt*1e3:.2f} "
           f"us/line={dt*1e6/prob.grid.ny:.1f} res={h[-1]:.3e}", flush=True)
+
+if not ref and "--perline" in sys.argv:
+    # per-line factorization path: the upwind closure makes the lines differ
+    from paper_2008_03276_b200.tvdcd import ConvectionDiffusionProblem
+    for iv in (128, 512):
+        q, _ = quartic_test_problem(iv, KappaSchemeConfig(kappa=1 / 3, eps=1e-6))
+        prob = ConvectionDiffusionProblem(q.grid, q.cfg, q.f, q.boundary, closure="upwind")
+        solve_by_sweeps(prob, "Ls1", tol=0.0, max_sweeps=1, cycle="x")
+        t = time.perf_counter()
+        _, h = solve_by_sweeps(prob, "Ls1", tol=0.0, max_sweeps=3, cycle="x")
+        dt = (time.perf_counter() - t) / 3
+        print(f"gpu per-line (upwind) intervals={iv} ms/sweep={dt*1e3:.2f} "
+              f"us/line={dt*1e6/prob.grid.ny:.1f} res={h[-1]:.3e}", flush=True)
