@@ -51,6 +51,19 @@ int paqif_tvd_sweep(const paqif_tvd_problem *p, double *u_full, int32_t backward
                     void *stream);
 size_t paqif_tvd_resid_bytes(int32_t nx, int32_t ny);
 
+/* sweep_splitting(problem, u, "Ls3", omega) (tvdcd.py:615-656): every
+ * x-line's change from the current iterate (one CTA per line), then
+ * u += omega (sigma - spread / 4) and residual_norm(u_next) into norm [dev].
+ * a_over_h [dev] ny x nx = a / h; line_bands [dev] 5 planes (offsets -2..2
+ * of the distributive line operator); k1 = (1 + kappa) / 4, k2 =
+ * (1 - kappa) / 4; sigma [dev] ny x nx and line_status [dev] ny scratch;
+ * status [dev] 1: 0 or 1 + the first line whose factorization broke down
+ * (then u_full is unchanged). */
+int paqif_tvd_distributive(const paqif_tvd_problem *p, double *u_full, const double *a_over_h,
+                           const double *line_bands, double k1, double k2, double *sigma,
+                           int32_t *line_status, double *resid, double *norm, int32_t *status,
+                           void *stream);
+
 /* Interior of src_full (ny+4) x (nx+4) into the interior of dst_full
  * (nx+4) x (ny+4), transposed: the hand-over to transposed_problem's twin
  * (tvdcd.py:492-511, solve_by_sweeps' "t" passes). */

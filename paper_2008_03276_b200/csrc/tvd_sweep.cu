@@ -418,6 +418,96 @@ __global__ void tvd_transpose_kernel(const double* src, int ny, int nx, double* 
   }
 }
 
+// Ls3 line-distributive relaxation (tvdcd.py:615-656): every x-line's
+// change from the current iterate -- independent lines, one CTA each:
+//   rhs = resid[j] + (a/h)[j] * (k1 (u[i+1] - u[i]) - k2 (u[i-1] - u[i-2])),
+//         explicit term 0 at i = 0
+//   sigma[j] = AQIF solve of the padded pentadiagonal line (offsets -2..2)
+__global__ void __launch_bounds__(kTvdThreads, 1)
+tvd_distributive_lines_kernel(paqif_tvd_problem p, const double* uf, const double* ah,
+                              const double* db, double k1, double k2, double* sigma,
+                              int32_t* status) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int flag;
+  const int nx = p.nx, ny = p.ny, W = nx + 4, j = blockIdx.x;
+  const int n = (nx + 1) % 2 == 0 ? nx + 1 : nx + 2;
+  const size_t plane = (size_t)nx * ny;
+  double* band = dsm;
+  double* rhs = band + aqif2_band_doubles(n);
+  double* rec = rhs + aqif2_rhs_doubles(n);
+  double* x = rec + (size_t)(n / 2 + 1) * kRec2;
+  aqif2_zero_pads(band, rhs, n);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
+    double rr = 0.0;
+    if (r < nx) {
+      const size_t k = (size_t)j * nx + r;
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        if (r + d - 2 >= 0) e[d] = db[d * plane + k];
+      const double* c = uf + (size_t)(2 + j) * W + 2 + r;
+      const double res = p.f[k] - apply_at(p, uf, j, r);
+      double ex = __dsub_rn(dmul(k1, __dsub_rn(c[1], c[0])), dmul(k2, __dsub_rn(c[-1], c[-2])));
+      if (r == 0) ex = 0.0;
+      rr = dadd(res, dmul(ah[k], ex));
+    }
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      const int col = r + d - 2;
+      band2_ref(band, n, r, d - 2) = (col >= 0 && col < n) ? e[d] : 0.0;
+    }
+    rhs[kBandPad + r] = rr;
+  }
+  const int st = aqif2_solve<true>(band, rhs, n, rec, x, &flag);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) sigma[(size_t)j * nx + i] = x[i];
+  if (threadIdx.x == 0) status[j] = (st & 1) ? 1 : 0;
+}
+
+// u += omega (sigma - 0.25 spread), spread = the four neighbours' sigma
+// (added left, right, below, above, as the reference's slices do), then
+// the residual norm; one CTA
+__global__ void __launch_bounds__(kTvdThreads, 1)
+tvd_distributive_update_kernel(paqif_tvd_problem p, double* uf, const double* sigma,
+                               const int32_t* lst, double* resid, double* norm,
+                               int32_t* status) {
+  const int nx = p.nx, ny = p.ny, W = nx + 4;
+  const size_t plane = (size_t)nx * ny;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < ny; j += blockDim.x)
+    if (lst[j]) atomicMax(&bad, j + 1);
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) *status = bad;  // a line broke down (the first is reported below)
+    for (int j = 0; j < ny && threadIdx.x == 0; ++j)
+      if (lst[j]) { *status = j + 1; break; }
+    return;
+  }
+  for (int64_t k = threadIdx.x; k < (int64_t)plane; k += blockDim.x) {
+    const int j = (int)(k / nx), i = (int)(k - (int64_t)j * nx);
+    double sp = 0.0;
+    if (i > 0) sp = dadd(sp, sigma[k - 1]);
+    if (i < nx - 1) sp = dadd(sp, sigma[k + 1]);
+    if (j > 0) sp = dadd(sp, sigma[k - nx]);
+    if (j < ny - 1) sp = dadd(sp, sigma[k + nx]);
+    double* c = uf + (size_t)(2 + j) * W + 2 + i;
+    *c = dadd(*c, dmul(p.omega, __dsub_rn(sigma[k], dmul(0.25, sp))));
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < (int64_t)plane; k += blockDim.x) {
+    const int j = (int)(k / nx), i = (int)(k - (int64_t)j * nx);
+    const double r = p.f[k] - apply_at(p, uf, j, i);
+    resid[k] = dmul(r, r);
+  }
+  __syncthreads();
+  const double sum = pairwise_sum_cta(resid, (int64_t)plane);
+  if (threadIdx.x == 0) {
+    *norm = sqrt(dmul(p.h2, sum));
+    *status = 0;
+  }
+}
+
 size_t tvd_smem(int nx, int zf_beta) {
   const int n = (nx + 1) % 2 == 0 ? nx + 1 : nx + 2;
   const size_t fz =
@@ -462,4 +552,27 @@ extern "C" int paqif_tvd_transpose(const double* src_full, int32_t ny, int32_t n
   dim3 grid((nx + 31) / 32, (ny + 31) / 32), block(32, 8);
   tvd_transpose_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(src_full, ny, nx, dst_full);
   return check_launch("paqif_tvd_transpose");
+}
+
+extern "C" int paqif_tvd_distributive(const paqif_tvd_problem* p, double* u_full,
+                                      const double* a_over_h, const double* line_bands,
+                                      double k1, double k2, double* sigma, int32_t* line_status,
+                                      double* resid, double* norm, int32_t* status, void* stream) {
+  if (!p || p->nx < 2 || p->ny < 1 || !p->f || !p->c0 || !u_full || !a_over_h || !line_bands ||
+      !sigma || !line_status || !resid || !norm || !status || p->kx < 0 || p->kx > 4 ||
+      p->ky < 0 || p->ky > 4 || (p->kx && !p->cx) || (p->ky && !p->cy))
+    return set_arg_error("paqif_tvd_distributive: problem / buffers");
+  const int n = (p->nx + 1) % 2 == 0 ? p->nx + 1 : p->nx + 2;
+  const size_t smem = (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) +
+                       (size_t)(n / 2 + 1) * kRec2 + n) * 8;
+  if (smem > 227 * 1024) return set_arg_error("paqif_tvd_distributive: line too long");
+  cudaFuncSetAttribute(tvd_distributive_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  cudaStream_t st = (cudaStream_t)stream;
+  tvd_distributive_lines_kernel<<<p->ny, kTvdThreads, smem, st>>>(*p, u_full, a_over_h, line_bands,
+                                                                 k1, k2, sigma, line_status);
+  if (int rc = check_launch("paqif_tvd_distributive")) return rc;
+  tvd_distributive_update_kernel<<<1, kTvdThreads, 0, st>>>(*p, u_full, sigma, line_status, resid,
+                                                            norm, status);
+  return check_launch("paqif_tvd_distributive");
 }

@@ -14,9 +14,11 @@ varying coefficients are factored one by one on the beta = 2 latency
 engine; constant-coefficient lines share one factorization, as in the
 reference, and each line is then only W and Z solves.
 
-Variants on the device: Ls0, Ls1, Ls2.  DefC (a sparse direct first-order
-solve, tvdcd.py:553-570) and Ls3 (documented as not robust,
-tvdcd.py:615-656) are not on the device path and raise NotImplementedError.
+Variants on the device: Ls0, Ls1, Ls2 (Gauss-Seidel line sweeps) and Ls3
+(the line-distributive relaxation, tvdcd.py:615-656: all lines' changes
+from the current iterate, one CTA per line).  DefC (a sparse direct
+first-order solve, tvdcd.py:553-570) is not on the device path and raises
+NotImplementedError.
 """
 
 from __future__ import annotations
@@ -301,6 +303,9 @@ def _lib():
         L.paqif_tvd_sweep.restype = _ct.c_int
         L.paqif_tvd_transpose.argtypes = [vp, _ct.c_int32, _ct.c_int32, vp, vp]
         L.paqif_tvd_transpose.restype = _ct.c_int
+        L.paqif_tvd_distributive.argtypes = [_ct.POINTER(_TvdProblem), vp, vp, vp, _ct.c_double,
+                                             _ct.c_double, vp, vp, vp, vp, vp, vp]
+        L.paqif_tvd_distributive.restype = _ct.c_int
         L._tvd_bound = True
     return L
 
@@ -312,7 +317,8 @@ class _DeviceSplitting:
     def __init__(self, problem: ConvectionDiffusionProblem, variant: str, omega: float):
         from . import _native
         torch = _native.torch_cuda()
-        bands = _line_system_coeffs(problem, variant)
+        self.variant = variant
+        bands = _line_system_coeffs(problem, "Ls1" if variant == "Ls3" else variant)
         op = problem.operator
         ny, nx = problem.f.shape
         if len(op.cx) > 4 or len(op.cy) > 4 or any(abs(o) > 2 for o in list(op.cx) + list(op.cy)):
@@ -342,11 +348,13 @@ class _DeviceSplitting:
         s.f, s.c0, s.cx, s.cy, s.lb = (self.f.data_ptr(), self.c0.data_ptr(),
                                        self.cx.data_ptr(), self.cy.data_ptr(),
                                        self.lb.data_ptr())
+        if variant == "Ls3":
+            self._distributive_setup(problem, dev)
         # constant-coefficient problems share one line factorization, as
         # the reference caches it (tvdcd.py:466-477): factored once
         # (paqif_factor_batch), each line then only solve_w + solve_z
         cfg = problem.cfg
-        if not (callable(cfg.a) or callable(cfg.b)) and all(
+        if variant != "Ls3" and not (callable(cfg.a) or callable(cfg.b)) and all(
                 np.ptp(c, axis=0).max() == 0.0 for c in bands.values()):
             from .aqif import factorize_wz
             beta = 2 if -2 in bands else 1
@@ -357,9 +365,40 @@ class _DeviceSplitting:
         self.struct = s
         self.shape = (ny, nx)
 
+    def _distributive_setup(self, problem, dev):
+        """Ls3's line operator and explicit-term weights
+        (tvdcd.py:615-645), per node; they do not depend on the iterate."""
+        from . import _native
+        torch = _native.torch_cuda()
+        grid, cfg = problem.grid, problem.cfg
+        h, k, eps = grid.h, cfg.kappa, cfg.eps
+        gx, gy = grid.interior_mesh()
+        a = cfg.a_field(gx, gy)
+        ny, nx = a.shape
+        a_pad = np.pad(a, ((0, 0), (1, 1)), mode="edge")
+        a_p = 0.5 * (a_pad[:, 1:-1] + a_pad[:, 2:])
+        a_m = 0.5 * (a_pad[:, 1:-1] + a_pad[:, :-2])
+        cm2 = eps / (4 * h ** 2) + a_m * (2 + k) / (8 * h)
+        cm1 = -(7 * eps / (4 * h ** 2) + a_p * (2 + k) / (2 * h) + a_m * (2 + k) / (8 * h))
+        c0 = 20 * eps / (4 * h ** 2) + a_p * (2 + k) / (2 * h) + a_m * (2 + k) / (8 * h)
+        cp1 = -(8 * eps / (4 * h ** 2) + a_p * (2 + k) / (2 * h))
+        cp2 = np.full((ny, nx), eps / (4 * h ** 2))
+        self.db = dev(np.stack([cm2, cm1, c0, cp1, cp2]))
+        self.ah = dev(a / h)
+        self.k12 = ((1 + k) / 4.0, (1 - k) / 4.0)
+        self.sigma = torch.empty((ny, nx), dtype=torch.float64, device="cuda")
+        self.lst = torch.zeros(ny, dtype=torch.int32, device="cuda")
+
     def sweep(self, u_full, backward: bool, want_norm: bool) -> None:
         from . import _native
         L = _lib()
+        if self.variant == "Ls3":
+            _native.check(L.paqif_tvd_distributive(
+                _ct.byref(self.struct), u_full.data_ptr(), self.ah.data_ptr(), self.db.data_ptr(),
+                self.k12[0], self.k12[1], self.sigma.data_ptr(), self.lst.data_ptr(),
+                self.resid.data_ptr(), self.scal.data_ptr(), self.status.data_ptr(),
+                _native.stream_ptr()), "paqif_tvd_distributive")
+            return
         _native.check(L.paqif_tvd_sweep(_ct.byref(self.struct), u_full.data_ptr(),
                                         1 if backward else 0, 1 if want_norm else 0,
                                         self.resid.data_ptr(), self.scal.data_ptr(),
@@ -373,10 +412,10 @@ class _DeviceSplitting:
 
 
 def _device_splitting(problem, variant, omega) -> _DeviceSplitting:
-    if variant == "DefC" or variant == "Ls3":
+    if variant == "DefC":
         raise NotImplementedError(
-            f"{variant} is not on the device path (DefC: sparse direct first-order solve; "
-            "Ls3: distributive variant) -- see DESIGN.md")
+            "DefC (the sparse direct first-order baseline) is not on the device path "
+            "-- see DESIGN.md")
     key = (variant, float(omega))
     d = problem._device.get(key)
     if d is None:

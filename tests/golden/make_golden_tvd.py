@@ -79,6 +79,27 @@ def main():
         out[f"{name}__f"], out[f"{name}__boundary"], out[f"{name}__u0"] = f, boundary, u0
         out[f"{name}__u1"], out[f"{name}__u2"] = u1, u2
         out[f"{name}__res"] = np.array([r1, r2])
+    # Ls3 (line-distributive relaxation): the reference's smoke setting and
+    # a variable-field custom problem, sweep by sweep, and an alternate cycle
+    cfg = KappaSchemeConfig(kappa=0.0, eps=1.0)
+    prob, _ = quartic_test_problem(16, cfg)
+    u = np.zeros_like(prob.f)
+    for k in range(3):
+        u, r = sweep_splitting(prob, u, "Ls3", omega=0.7)
+        out[f"ls3_q16__u{k}"], out[f"ls3_q16__r{k}"] = u, np.array(r)
+    u, hist = solve_by_sweeps(prob, "Ls3", omega=0.7, tol=0.0, max_sweeps=3, cycle="alternate")
+    out["ls3_q16_alt__u"], out["ls3_q16_alt__hist"] = u, np.array(hist)
+    rng = np.random.default_rng(7)
+    grid = Grid2D(-1.0, 1.0, -1.0, 1.0, 21, 21)
+    cfg = KappaSchemeConfig(kappa=1.0 / 3.0, eps=0.5, a=field_a, b=field_b)
+    f = rng.standard_normal((21, 21))
+    boundary = rng.standard_normal((25, 25))
+    prob = ConvectionDiffusionProblem(grid, cfg, f, boundary, closure="upwind")
+    u0 = rng.standard_normal((21, 21))
+    u1, r1 = sweep_splitting(prob, u0, "Ls3", omega=0.6)
+    u2, r2 = sweep_splitting(prob, u1, "Ls3", omega=0.6)
+    out.update({"ls3_var__f": f, "ls3_var__boundary": boundary, "ls3_var__u0": u0,
+                "ls3_var__u1": u1, "ls3_var__u2": u2, "ls3_var__res": np.array([r1, r2])})
     np.savez_compressed(os.path.join(HERE, "tvd.npz"), **out)
 
 

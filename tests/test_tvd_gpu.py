@@ -105,6 +105,45 @@ def test_residual_gate_and_errors():
         sweep_splitting(prob, exact, "DefC")
 
 
+def test_distributive_ls3_vs_reference():
+    # Ls3 line-distributive relaxation (tvdcd.py:615-656), bit-exact: the
+    # reference's smoke setting sweep by sweep and through an alternate
+    # cycle, and a variable-field upwind-closure problem
+    from paper_2008_03276_b200.tvdcd import (ConvectionDiffusionProblem, Grid2D,
+                                             KappaSchemeConfig, quartic_test_problem,
+                                             solve_by_sweeps, sweep_splitting)
+    prob, _ = quartic_test_problem(16, KappaSchemeConfig(kappa=0.0, eps=1.0))
+    u = np.zeros_like(prob.f)
+    for k in range(3):
+        u, r = sweep_splitting(prob, u, "Ls3", omega=0.7)
+        assert np.array_equal(_bits(u), _bits(T[f"ls3_q16__u{k}"]))
+        assert np.array_equal(_bits([r]), _bits([T[f"ls3_q16__r{k}"]]))
+    u, hist = solve_by_sweeps(prob, "Ls3", omega=0.7, tol=0.0, max_sweeps=3, cycle="alternate")
+    assert np.array_equal(_bits(u), _bits(T["ls3_q16_alt__u"]))
+    assert np.array_equal(_bits(hist), _bits(T["ls3_q16_alt__hist"]))
+    cfg = KappaSchemeConfig(kappa=1.0 / 3.0, eps=0.5, a=field_a, b=field_b)
+    prob = ConvectionDiffusionProblem(Grid2D(-1.0, 1.0, -1.0, 1.0, 21, 21), cfg, T["ls3_var__f"],
+                                      T["ls3_var__boundary"], closure="upwind")
+    u1, r1 = sweep_splitting(prob, T["ls3_var__u0"], "Ls3", omega=0.6)
+    u2, r2 = sweep_splitting(prob, u1, "Ls3", omega=0.6)
+    assert np.array_equal(_bits(u1), _bits(T["ls3_var__u1"]))
+    assert np.array_equal(_bits(u2), _bits(T["ls3_var__u2"]))
+    assert np.array_equal(_bits([r1, r2]), _bits(T["ls3_var__res"]))
+
+
+def test_distributive_ls3_progress():
+    # the reference's smoke gate (tests/test_tvdcd.py): 30 under-relaxed
+    # sweeps do not blow up and make progress
+    from paper_2008_03276_b200.tvdcd import KappaSchemeConfig, quartic_test_problem, sweep_splitting
+    prob, _ = quartic_test_problem(16, KappaSchemeConfig(kappa=0.0, eps=1.0))
+    u = np.zeros_like(prob.f)
+    first = None
+    for _ in range(30):
+        u, res = sweep_splitting(prob, u, "Ls3", omega=0.7)
+        first = first if first is not None else res
+    assert res < first
+
+
 def test_large_grid_sweep_consistent():
     # size-independent property at a study-scale grid: the device residual
     # norm equals the host restatement's on the device iterate
