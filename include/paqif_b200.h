@@ -132,7 +132,9 @@ size_t paqif_lcp_workspace_bytes(int64_t B, int64_t n, int64_t beta);
  * same active-set policy, same pass count, same termination rules.
  * Outputs: u (B,n) solution, active (B,n) uint8 pinned set of the returned
  * pass, passes (B,) int64, res (B,) final complementarity residual,
- * status (B,) int64 PAQIF_LCP_*. */
+ * status (B,) int64 PAQIF_LCP_*.  On a breakdown (status 1 or 2) res[b]
+ * holds -(the 1-based breakdown level), which the Python layer passes on as
+ * FactorizationBreakdownError.level (aqif.py:133-134, 174-175). */
 int paqif_lcp_batch(int64_t B, int64_t n, int64_t beta, const double *bands /*[dev]*/,
                     const double *f /*[dev]*/, double tol, int64_t max_outer, uint32_t flags,
                     double *u /*[dev]*/, uint8_t *active /*[dev]*/, int64_t *passes /*[dev]*/,

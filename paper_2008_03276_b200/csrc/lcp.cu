@@ -265,7 +265,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       }
     }
     double best_res = INFINITY, res = INFINITY;
-    int passes = 0, st = 0;
+    int passes = 0, st = 0, brk_level = 0;
     bool done = false;
     bool active = have;  // this group still iterating
     uint32_t* cur = act;
@@ -293,6 +293,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       }
       if (fst) {
         st = PAQIF_LCP_FACTOR_BREAKDOWN;
+        brk_level = fst;
         active = false;
       }
       __syncwarp();
@@ -302,8 +303,9 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         active = false;
       }
       PAQIF_TSTAMP(t2);
-      if (zsolve_group<BETA, EXACT, false>(zs, n, x, my_sm.post.scratch, gl, active)) {
+      if (const int zst = zsolve_group<BETA, EXACT, false>(zs, n, x, my_sm.post.scratch, gl, active)) {
         st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
+        brk_level = zst;
         active = false;
       }
       PAQIF_TSTAMP(t3);
@@ -452,7 +454,8 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       for (int q = 0; q < 4; ++q) { atomicAdd(&g_phase_cycles[q], ph_acc[q]); ph_acc[q] = 0; }
 #endif
       if (passes_out) passes_out[b] = passes;
-      if (res_out) res_out[b] = res;
+      // a breakdown reports -(1-based level) in res (include/paqif_b200.h)
+      if (res_out) res_out[b] = brk_level ? -(double)brk_level : res;
       status_out[b] = st;
     }
     unsigned long long nx = 0;

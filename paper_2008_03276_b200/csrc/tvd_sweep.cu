@@ -377,15 +377,21 @@ tvd_sweep_kernel(paqif_tvd_problem p, double* uf, int backward, int want_norm, d
         }
         rhs[kBandPad + r] = rr;
       }
-      const int s = aqif2_solve<true>(band, rhs, n, rec, band, &flag);
+      // the solution goes to its own buffer: writing it over the band would
+      // clobber the diagonal -2 leading pads the next line's factor reads
+      double* xs = rec + (size_t)(n / 2 + 1) * kRec2;
+      const int s = aqif2_solve<true>(band, rhs, n, rec, xs, &flag);
       if (s & 1) {
         st = j + 1;
         break;
       }
     }
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-      double* c = uf + (size_t)(2 + j) * W + 2 + i;
-      *c = dadd(*c, dmul(p.omega, band[i]));
+    {
+      const double* xs = rec + (size_t)(n / 2 + 1) * kRec2;
+      for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+        double* c = uf + (size_t)(2 + j) * W + 2 + i;
+        *c = dadd(*c, dmul(p.omega, xs[i]));
+      }
     }
     __syncthreads();
   }
@@ -512,7 +518,7 @@ size_t tvd_smem(int nx, int zf_beta) {
   const int n = (nx + 1) % 2 == 0 ? nx + 1 : nx + 2;
   const size_t fz =
       zf_beta ? (size_t)(n / 2 + 1) * (4 + 4 * (zf_beta + 1) + 4 * zf_beta + 3) + 4 * (size_t)nx + 8
-              : 0;
+              : (size_t)n;  // per-line factors: the solution buffer
   return (aqif2_band_doubles(n) + aqif2_rhs_doubles(n) + (size_t)(n / 2 + 1) * kRec2 + fz) * 8;
 }
 

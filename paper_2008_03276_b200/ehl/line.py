@@ -9,7 +9,6 @@ iteration of solve_ehl per ``step()`` -- one fused kernel launch
 from __future__ import annotations
 
 import ctypes
-import math
 
 import numpy as np
 
@@ -210,19 +209,3 @@ def line_deformation(table, u):
     _native.check(rc, "paqif_line_deformation")
     out = to.cpu().numpy()
     return out[0] if one else out
-
-
-def smoke_line_step():
-    """__graft_entry__.smoke() hook: one config-1 line step vs the oracle."""
-    import oracle.ehl_oracle as E
-    from .params import moes_convert
-    u_, w_ = moes_convert(m=20.0, l=10.0, g=5000.0)
-    p = EhlParams.line_from_loads(5000.0, u_, w_, domain=(-4.5, 1.5))
-    batch = LineContactBatch([p], 512)
-    batch.step()
-    u, h0, film, res, _, info = batch.snapshot()
-    c = E.LineCase(p_hertz=p.p_hertz, lam=p.lam)
-    f = E.LineFilm(512, c)
-    ur, h0r, fr, rr, _ = E.line_step(E.hertz_start(c, f), c.h0, 0, c, f)
-    assert np.max(np.abs(u[0] - ur)) <= 1e-9 * max(1.0, np.max(np.abs(ur))), "line step parity"
-    assert math.isclose(res[0], rr, rel_tol=1e-9)

@@ -13,7 +13,6 @@ enqueued by a native host loop on the handle's stream.
 from __future__ import annotations
 
 import ctypes
-import math
 
 import numpy as np
 
@@ -274,22 +273,3 @@ class PointContact:
 
     def close(self) -> None:
         self._h.close()
-
-
-def smoke_point_step():
-    """__graft_entry__.smoke() hook: one small point step vs the oracle."""
-    import oracle.ehl_point_oracle as P
-    p = EhlParams.point_from_moes(100.0, 10.0, domain=(-4.5, 1.5), lo_y=-3.0)
-    n = 32
-    pc = PointContact(p, n)
-    pc.step()
-    got = pc.snapshot()
-    c = P.point_case(100.0, 10.0)
-    f = P.PointFilm(n, c)
-    u0 = P.hertz_start(c, f)
-    ur, h0r, fr, rr, info = P.point_step(u0, c.h0, 0, c, f)
-    scale = max(1.0, float(np.max(np.abs(ur))))
-    assert np.array_equal(got["newton"], np.asarray(info["tags"])), "x-sweep Newton tags"
-    assert np.max(np.abs(got["u"] - ur)) <= 1e-9 * scale, "point step parity"
-    assert math.isclose(got["res"], rr, rel_tol=1e-8, abs_tol=1e-12)
-    pc.close()

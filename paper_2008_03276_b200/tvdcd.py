@@ -181,7 +181,6 @@ class ConvectionDiffusionProblem:
 
     def __post_init__(self):
         self.operator = assemble_kappa_operator(self.cfg, self.grid, self.closure)
-        self._device = {}
 
     def embed(self, u: np.ndarray) -> np.ndarray:
         full = self.boundary.copy()
@@ -364,6 +363,15 @@ class _DeviceSplitting:
             s.zf_beta = beta
         self.struct = s
         self.shape = (ny, nx)
+        self._bands = bands
+        self._f_src = None
+
+    def refresh_f(self, f: np.ndarray) -> None:
+        """Re-upload the right side (the reference re-reads problem.f on
+        every line, so edits between calls must be seen)."""
+        from . import _native
+        torch = _native.torch_cuda()
+        self.f.copy_(torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)))
 
     def _distributive_setup(self, problem, dev):
         """Ls3's line operator and explicit-term weights
@@ -408,7 +416,28 @@ class _DeviceSplitting:
     def check_status(self) -> None:
         st = int(self.status.item())
         if st:
-            raise FactorizationBreakdownError(st - 1, f"x-line {st - 1}: AQIF breakdown")
+            j = st - 1
+            raise FactorizationBreakdownError(self._breakdown_level(j),
+                                              f"x-line {j}: AQIF breakdown")
+
+    def _breakdown_level(self, j: int) -> int:
+        """1-based level at which line j's factorization breaks down (the
+        reference's FactorizationBreakdownError.level), from the device
+        engine on that line's matrix; error path only."""
+        from .aqif import factorize_wz
+        nx = self.shape[1]
+        if self.variant == "Ls3":
+            db = self.db.cpu().numpy()
+            rows = {o: db[o + 2, j] for o in range(-2, 3)}
+            beta = 2
+        else:
+            rows = {o: c[j] for o, c in self._bands.items()}
+            beta = 2 if -2 in rows else 1
+        try:
+            factorize_wz(_line_matrix(rows, nx, beta))
+        except FactorizationBreakdownError as exc:
+            return exc.level
+        return -1  # the Z solve broke down, not the factorization
 
 
 def _device_splitting(problem, variant, omega) -> _DeviceSplitting:
@@ -416,10 +445,14 @@ def _device_splitting(problem, variant, omega) -> _DeviceSplitting:
         raise NotImplementedError(
             "DefC (the sparse direct first-order baseline) is not on the device path "
             "-- see DESIGN.md")
-    key = (variant, float(omega))
-    d = problem._device.get(key)
+    # keyed on the operator object too: a problem whose operator / grid was
+    # replaced gets fresh device planes; f is re-uploaded on every call
+    cache = problem.__dict__.setdefault("_device", {})
+    key = (variant, float(omega), id(problem.operator), problem.closure, problem.f.shape)
+    d = cache.get(key)
     if d is None:
-        d = problem._device[key] = _DeviceSplitting(problem, variant, omega)
+        d = cache[key] = _DeviceSplitting(problem, variant, omega)
+    d.refresh_f(problem.f)
     return d
 
 
@@ -464,9 +497,7 @@ def solve_by_sweeps(problem: ConvectionDiffusionProblem, variant: str, omega: fl
     uf = torch.from_numpy(problem.embed(u)).cuda()
     twin = dt = uft = None
     if any(p.startswith("t") for p in seq):
-        if not hasattr(problem, "_twin"):
-            problem._twin = transposed_problem(problem)
-        twin = problem._twin
+        twin = transposed_problem(problem)  # per call, as the reference builds it
         dt = _device_splitting(twin, variant, omega)
         uft = torch.from_numpy(np.ascontiguousarray(twin.boundary)).cuda()
     history = []

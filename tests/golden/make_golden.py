@@ -11,6 +11,7 @@ Outputs (committed, small):
                                   solve_z_batch / band_matvec_batch outputs
   tests/golden/lcp.npz            paqif_solve_lcp(r=1) on seeded systems
   tests/golden/paqif_r.npz        paqif_solve(L, f, r) for r in {1,2,4,8}
+  tests/golden/paqif_proj.npz     paqif_solve(L, f, r, project=True)
 The EHL goldens are produced by make_golden_ehl.py.
 """
 
@@ -193,7 +194,28 @@ def paqif_r_cases():
     return out
 
 
+def paqif_project_cases():
+    """paqif_solve(L, f, r, project=True): corners projected before the
+    middles' Z solve, middles projected (parallel.py:278-289)."""
+    rng = np.random.default_rng(7)
+    out = {}
+    k = 0
+    for n, beta, r in [(128, 2, 4), (96, 3, 4), (256, 8, 8), (64, 1, 8), (160, 5, 2)]:
+        for _ in range(2):
+            bands = random_banded(n, beta, rng)
+            f = rng.standard_normal(n)
+            u = paqif_solve(BandedMatrix(n, beta, bands), f, r, project=True)
+            out[f"p{k}__bands"] = bands; out[f"p{k}__f"] = f; out[f"p{k}__u"] = u
+            out[f"p{k}__r"] = np.int64(r)
+            k += 1
+    return out
+
+
 def main():
+    if "--project-only" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "paqif_proj.npz"), **paqif_project_cases())
+        return
+    np.savez_compressed(os.path.join(HERE, "paqif_proj.npz"), **paqif_project_cases())
     np.savez_compressed(os.path.join(HERE, "aqif_kernels.npz"), **flatten(aqif_cases()))
     np.savez_compressed(os.path.join(HERE, "lcp.npz"), **lcp_cases())
     np.savez_compressed(os.path.join(HERE, "paqif_r.npz"), **paqif_r_cases())

@@ -211,29 +211,19 @@ class TestRblockDevice:
             ud = np.linalg.solve(l.to_dense(), f[b])
             assert np.max(np.abs(x[b] - ud)) <= 1e-12 * max(1.0, np.max(np.abs(ud)))
 
-    def test_project_flag(self, rng):
-        """project=True against the host restatement of the seven steps
-        (parallel.py's step functions: numpy reduced system, projection of
-        the corners, middles from the projected corners, projection)."""
-        from paper_2008_03276_b200 import BandedMatrix, parallel
-        from paper_2008_03276_b200.batch import solve_rblock_batch
-        from paper_2008_03276_b200.bandcore import project_nonneg
-        from paper_2008_03276_b200.workloads import lcp_batch as gen
-        n, beta, r = 128, 2, 4
-        bands, f = gen(3, 4, n=n, beta=beta)
-        x1, st = solve_rblock_batch(bands, f, r, project=True)
-        assert np.all(st == 0) and np.all(x1 >= 0.0)
-        for b in range(bands.shape[0]):
-            part = parallel.partition(BandedMatrix(n, beta, bands[b]), f[b], r)
-            data = parallel._forward_all(part)
-            ud = project_nonneg(parallel.solve_reduced(parallel.build_reduced_system(part, data)))
-            t = part.block_size
-            bnd = [(ud[2 * beta * m:2 * beta * m + beta], ud[2 * beta * m + beta:2 * beta * (m + 1)])
-                   for m in range(r)]
-            mids = parallel.back_substitute_middle(part, data, bnd)
-            ref = np.concatenate([np.r_[u[:beta], project_nonneg(u[beta:t - beta]), u[t - beta:]]
-                                  for u, _, _ in mids])
-            assert np.max(np.abs(x1[b] - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    @pytest.mark.parametrize("case", range(len(golden_cases("paqif_proj.npz", "__"))))
+    def test_project_flag_vs_reference(self, case):
+        """project=True against the reference's paqif_solve(..., project=True)
+        (tests/golden/paqif_proj.npz, make_golden.py)."""
+        from paper_2008_03276_b200 import BandedMatrix
+        from paper_2008_03276_b200.parallel import paqif_solve
+        G = golden_cases("paqif_proj.npz")[case]
+        bands = G["bands"]
+        l = BandedMatrix(bands.shape[1], (bands.shape[0] - 1) // 2, bands)
+        u = paqif_solve(l, G["f"], int(G["r"]), project=True)
+        ref = G["u"]
+        assert np.max(np.abs(u - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+        assert np.array_equal(u[ref == 0.0] == 0.0, np.ones(int((ref == 0.0).sum()), bool))
 
     def test_statuses(self):
         from paper_2008_03276_b200.batch import solve_rblock_batch
@@ -246,13 +236,15 @@ class TestRblockDevice:
         assert int(st[0]) == LCP_FACTOR_BREAKDOWN
 
     def test_no_host_reduced_system(self, monkeypatch):
-        """The public paqif_solve(r>1) does not touch the host step functions."""
+        """The public paqif_solve(r>1) runs on the device: no host linear
+        algebra is reachable from it (numpy.linalg / scipy patched to fail)."""
+        import scipy.linalg
         from paper_2008_03276_b200 import BandedMatrix, parallel
         def boom(*a, **k):
             raise AssertionError("host path used")
-        for name in ("_forward_all", "build_reduced_system", "solve_reduced",
-                     "back_substitute_middle"):
-            monkeypatch.setattr(parallel, name, boom)
+        for mod, name in ((np.linalg, "inv"), (np.linalg, "solve"), (scipy.linalg, "cho_factor"),
+                          (scipy.linalg, "cho_solve")):
+            monkeypatch.setattr(mod, name, boom)
         rng = np.random.default_rng(5)
         n = 128
         l = BandedMatrix.from_diagonals(n, {-1: -1.0, 0: 4.0, 1: -1.0})

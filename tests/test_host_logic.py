@@ -12,7 +12,7 @@ from paper_2008_03276_b200.bandcore import (BandedMatrix, band_matvec, cholesky_
                                             is_diagonally_dominant, project_nonneg)
 from paper_2008_03276_b200.errors import (ContractViolationError, NotPositiveDefiniteError,
                                           PartitionError)
-from paper_2008_03276_b200.parallel import CostModel, partition, predict_speedup
+from paper_2008_03276_b200.parallel import CostModel, check_partition, predict_speedup
 from paper_2008_03276_b200.workloads import lcp_batch, lcp_system, random_banded
 
 
@@ -60,22 +60,35 @@ def test_cholesky(rng):
 
 
 class TestPartition:
-    def test_reassembly_bit_exact(self, rng):
-        l = BandedMatrix(32, 2, random_banded(32, 2, rng))
-        p = partition(l, rng.standard_normal(32), 4)
-        assert np.array_equal(p.reassemble().bands, l.bands)
+    """Block-split validation of paqif_solve(l, f, r): the reference's
+    partition checks (parallel.py:106-125), same types, same order."""
 
-    def test_errors(self, rng):
-        l = BandedMatrix(16, 2, random_banded(16, 2, rng))
-        with pytest.raises(PartitionError):
-            partition(l, np.zeros(16), 3)
-        with pytest.raises(PartitionError):
-            partition(l, np.zeros(16), 4)
+    def test_block_size(self):
+        assert check_partition(32, 2, 4) == 8
+        assert check_partition(1026, 8, 1) == 1026
 
-    def test_tridiag_coupling(self):
-        l = BandedMatrix.from_diagonals(8, {-1: -1.0, 0: 2.0, 1: -1.0})
-        p = partition(l, np.zeros(8), 2)
-        assert p.lplus[0][0, 0] == -1.0 and p.lminus[1][0, 0] == -1.0
+    def test_errors(self):
+        with pytest.raises(PartitionError):
+            check_partition(16, 2, 3)      # does not divide
+        with pytest.raises(PartitionError):
+            check_partition(16, 2, 4)      # t = 4 <= 2 beta
+        with pytest.raises(PartitionError):
+            check_partition(18, 1, 2)      # t = 9 odd
+        with pytest.raises(PartitionError):
+            check_partition(16, 2, 0)
+        with pytest.raises(ContractViolationError):
+            check_partition(16, 2, 2, rhs_len=15)
+
+    def test_wide_band_rejected(self):
+        """beta > 16 has no device engine: rejected before any compute (no
+        host fallback)."""
+        from paper_2008_03276_b200.parallel import paqif_solve, paqif_solve_lcp
+        from paper_2008_03276_b200.lcp import LcpProblem
+        l = BandedMatrix.identity(80, 17)
+        with pytest.raises(ContractViolationError):
+            paqif_solve(l, np.ones(80), 1)
+        with pytest.raises(ContractViolationError):
+            paqif_solve_lcp(LcpProblem(l, np.ones(80)), 1)
 
 
 class TestCostModel:

@@ -118,6 +118,20 @@ def test_lcp_edge_cases():
     ff[1] = 1.0
     r = lcp_batch(bb, ff)
     assert r.status[1] == 1 and r.status[0] == 0 and r.status[2] == 0
+    assert r.res[1] == -1.0  # a breakdown reports -(1-based level) in res
+    # ... which the API raises as FactorizationBreakdownError.level
+    from paper_2008_03276_b200 import BandedMatrix, FactorizationBreakdownError
+    from paper_2008_03276_b200.lcp import LcpProblem
+    from paper_2008_03276_b200.parallel import paqif_solve, paqif_solve_lcp
+    d = np.ones(64)
+    d[5] = 0.0  # the level-27 corner (rows 5, 58) is singular: the reference
+    l = BandedMatrix.from_diagonals(64, {0: d, 1: np.zeros(63)})  # raises level=27
+    with pytest.raises(FactorizationBreakdownError) as ei:
+        paqif_solve_lcp(LcpProblem(l, np.ones(64)), 1)
+    assert ei.value.level == 27
+    with pytest.raises(FactorizationBreakdownError) as ei:
+        paqif_solve(l, np.ones(64), 1)
+    assert ei.value.level == 27
 
 
 def test_solve_r1_matches_oracle():
