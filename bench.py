@@ -9,7 +9,11 @@ solve paqif_solve_lcp(r=1) on every system of the batch (2-4 factor + W + Z
 passes each).  Rank r solves systems [4096 r, 4096 (r+1)) -- no collective on
 the data path; NCCL only carries the max-over-ranks timing.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--fast]
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--exact]
+
+--gpus N > 1 without WORLD_SIZE in the environment re-launches itself under
+torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1); under a
+launcher WORLD_SIZE must equal N.
 
 Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream,
 barrier + synchronize on both sides, max over ranks; inputs (571 MB of bands
@@ -50,10 +54,12 @@ def load_peaks():
         peaks["hbm_gbs"] = float(d.get("hbm_gbs", peaks["hbm_gbs"]))
         peaks["src"] = "MEASURED_PEAKS.json"
     peaks["fp64_tflops"] = 33.94  # DFMA microbenchmark, profiles/peaks_r01.json
+    peaks["fp64_src"] = "tools/peaks.cu DFMA microbenchmark (fallback constant)"
     p2 = os.path.join(ROOT, "profiles", "peaks_r01.json")
     if os.path.exists(p2):
         with open(p2) as fh:
             peaks["fp64_tflops"] = float(json.load(fh)["dfma_tflops"])
+        peaks["fp64_src"] = "tools/peaks.cu DFMA microbenchmark (profiles/peaks_r01.json)"
     return peaks
 
 
@@ -168,20 +174,68 @@ def config3_cases(rank, count=1024, seed=SEED):
     return out
 
 
-def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1)):
+def config3_flops(n_int=1024):
+    """Algorithmic fp64 work of one config-3 case-iteration:
+    two N x N direct deformation convolutions (2 flop per MAC), one beta=2
+    AQIF factor + W + Z (the paper's CostModel count), ~200 flop per node
+    twice (rheology, faces, assembly, residual)."""
+    from paper_2008_03276_b200.parallel import CostModel
+    n = n_int + 1
+    return 2 * 2 * n * n + CostModel(n_int, 2, 1).serial_total() + 2 * 200 * n
+
+
+def _c3_cpu_worker(job):
+    """One host core: oracle line steps of config-3 case `c` for ~`secs`."""
+    c, m, l, secs = job
+    import oracle.ehl_oracle as E
+    p = _line_params(m, l)
+    case = E.LineCase(p_hertz=p.p_hertz, lam=p.lam)
+    film = E.LineFilm(1024, case)
+    u, h0 = E.hertz_start(case, film), case.h0
+    t0 = time.perf_counter()
+    k = 0
+    while k < 3 or time.perf_counter() - t0 < secs:
+        u, h0, _, _, _ = E.line_step(u, h0, k, case, film)
+        k += 1
+    return k, time.perf_counter() - t0
+
+
+def config3_cpu_pool(cases, threads, secs=4.0):
+    """Config-3 CPU baseline: a process pool over all host cores, each
+    worker running the numpy oracle's line steps on its own case (BLAS /
+    OpenMP threads pinned to 1 per worker).  Returns (case-iters/s, sample)."""
+    import multiprocessing as mp
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
+    jobs = [(c, m, l, secs) for c, (m, l) in enumerate(cases[:threads])]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(threads) as pool:
+        res = pool.map(_c3_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    steps = sum(k for k, _ in res)
+    busy = max(t for _, t in res)
+    return steps / busy, (f"{len(jobs)} cases x ~{secs:.0f} s of oracle line steps, one per "
+                          f"process ({steps} case-iterations, {wall:.1f} s wall incl. start-up)")
+
+
+def ehl_secondary(rank, world, with_cpu, max_over_ranks, barrier, steps1=200, steps3=5,
+                  point_steps=(3, 1)):
     """EHL Newton-step throughput: config 1 (one line contact, N=513) and
     config 3 (1024 line contacts per GPU, N=1025), device-timed per outer
-    iteration, plus the oracle CPU rate on this host."""
+    iteration, plus the oracle CPU rate on this host.  With several ranks
+    only the sharded config 3 runs (configs 1/4/5 and the TVD line are
+    single-GPU workloads: replicas only)."""
     import numpy as np
     import torch
     from paper_2008_03276_b200.ehl import LineContactBatch
     out = {}
     stream = torch.cuda.current_stream()
+    peaks = load_peaks()
 
     def timed(batch, k):
         for _ in range(3):
             batch.step()
-        torch.cuda.synchronize()
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -189,42 +243,54 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
             batch.step()
         e1.record(stream)
         e1.synchronize()
-        return e0.elapsed_time(e1) / k
+        return max_over_ranks(e0.elapsed_time(e1) / k)
 
     p1 = _line_params(20.0, 10.0)
-    ms1 = timed(LineContactBatch([p1], 512), steps1)
-    ms1f = timed(LineContactBatch([p1], 512, exact=False), steps1)
-    out["config1"] = {"metric": "EHL Newton iters/s (line, N=513, M=20, L=10, B=1)",
-                      "value": 1e3 / ms1, "unit": "iters/s", "us_per_iter": ms1 * 1e3,
-                      "gpu_launches_per_iter": 1,
-                      "fma": {"us_per_iter": ms1f * 1e3, "value": 1e3 / ms1f}}
-    # end to end through the public solve_ehl (device-side stop tests, one
-    # host synchronisation per 32 iterations; initial state uploaded, final
-    # state read back inside the timed region)
-    from paper_2008_03276_b200.ehl import solve_ehl
-    from paper_2008_03276_b200.errors import NonConvergenceError
-    k_e2e = max(steps1, 64)
-    for rep in range(2):  # first call warms the caches
-        t0 = time.perf_counter()
-        try:
-            solve_ehl(p1, 512, tol=0.0, tol_fb=0.0, max_outer=k_e2e)
-        except NonConvergenceError:
-            pass
-        dt = time.perf_counter() - t0
-    out["config1"]["e2e"] = {"value": k_e2e / dt, "unit": "iters/s",
-                             "path": f"solve_ehl(max_outer={k_e2e}), device-side stop tests",
-                             "h2d_bytes": 513 * 8 * 2, "d2h_bytes": 513 * 8 + 48}
+    if world == 1:
+        ms1 = timed(LineContactBatch([p1], 512), steps1)
+        ms1f = timed(LineContactBatch([p1], 512, exact=False), steps1)
+        out["config1"] = {"metric": "EHL Newton iters/s (line, N=513, M=20, L=10, B=1)",
+                          "value": 1e3 / ms1, "unit": "iters/s", "us_per_iter": ms1 * 1e3,
+                          "gpu_launches_per_iter": 1,
+                          "fma": {"us_per_iter": ms1f * 1e3, "value": 1e3 / ms1f}}
+        # end to end through the public solve_ehl (device-side stop tests, one
+        # host synchronisation per 32 iterations; initial state uploaded, final
+        # state read back inside the timed region)
+        from paper_2008_03276_b200.ehl import solve_ehl
+        from paper_2008_03276_b200.errors import NonConvergenceError
+        k_e2e = max(steps1, 64)
+        for rep in range(2):  # first call warms the caches
+            t0 = time.perf_counter()
+            try:
+                solve_ehl(p1, 512, tol=0.0, tol_fb=0.0, max_outer=k_e2e)
+            except NonConvergenceError:
+                pass
+            dt = time.perf_counter() - t0
+        out["config1"]["e2e"] = {"value": k_e2e / dt, "unit": "iters/s",
+                                 "path": f"solve_ehl(max_outer={k_e2e}), device-side stop tests",
+                                 "h2d_bytes": 513 * 8 * 2, "d2h_bytes": 513 * 8 + 48}
     cases = config3_cases(rank)
     b3 = LineContactBatch([_line_params(m, l) for m, l in cases], 1024)
     ms3 = timed(b3, steps3)
     info = b3.info.cpu().numpy()
     ms3f = timed(LineContactBatch([_line_params(m, l) for m, l in cases], 1024, exact=False),
                  steps3)
+    fl3 = config3_flops()
+    tf3 = len(cases) * fl3 / (ms3 * 1e-3) / 1e12
+    tf3f = len(cases) * fl3 / (ms3f * 1e-3) / 1e12
     out["config3"] = {"metric": "EHL line-contact case-iterations/s (1024 cases/GPU, N=1025)",
                       "value": world * len(cases) * 1e3 / ms3, "unit": "case-iters/s",
-                      "ms_per_iter": ms3, "scaling": "weak",
+                      "ms_per_iter": ms3, "scaling": "weak", "n_gpus": world,
                       "ladder_cases_last_iter": int(np.sum((info & 3) > 0)),
-                      "fma": {"ms_per_iter": ms3f, "value": world * len(cases) * 1e3 / ms3f}}
+                      "roofline": {"bound": "fp64", "achieved": tf3,
+                                   "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                                   "frac": tf3 / peaks["fp64_tflops"],
+                                   "flops_per_case_iter": fl3,
+                                   "count": "2 N^2-MAC deformations + CostModel(1024,2,1) "
+                                            "+ 400 flop/node (SURVEY.md 8(d))",
+                                   "peak_src": peaks["fp64_src"]},
+                      "fma": {"ms_per_iter": ms3f, "value": world * len(cases) * 1e3 / ms3f,
+                              "roofline_frac": tf3f / peaks["fp64_tflops"]}}
     if with_cpu:
         import oracle.ehl_oracle as E
         c = E.LineCase(p_hertz=p1.p_hertz, lam=p1.lam)
@@ -239,22 +305,16 @@ def ehl_secondary(rank, world, with_cpu, steps1=200, steps3=5, point_steps=(3, 1
         out["config1"]["cpu_baseline"] = {"value": 1.0 / dt, "unit": "iters/s", "cores": 1,
                                           "kind": "port",
                                           "sample": f"{k} oracle line steps (numpy restatement)"}
-        c3 = E.LineCase(p_hertz=b3.p_hertz[0].item(), lam=b3.lam[0].item())
-        f3 = E.LineFilm(1024, c3)
-        u3, h3 = E.hertz_start(c3, f3), c3.h0
-        t0 = time.perf_counter()
-        k = 0
-        while k < 5 or time.perf_counter() - t0 < 3.0:
-            u3, h3, _, _, _ = E.line_step(u3, h3, k, c3, f3)
-            k += 1
-        dt3 = (time.perf_counter() - t0) / k
-        out["config3"]["cpu_baseline"] = {"value": 1.0 / dt3, "unit": "case-iters/s",
-                                          "cores": 1, "kind": "port",
-                                          "sample": f"{k} oracle steps of case 0, one core"}
-    out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
+        threads = cpu_threads()
+        rate, sample = config3_cpu_pool(cases, threads)
+        out["config3"]["cpu_baseline"] = {"value": rate, "unit": "case-iters/s",
+                                          "cores": threads, "kind": "port", "sample": sample}
+    if world == 1:
+        out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
     for v in out.values():
         v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
-    out["tvd"] = tvd_secondary()
+    if world == 1:
+        out["tvd"] = tvd_secondary()
     return out
 
 
@@ -336,6 +396,94 @@ def point_secondary(with_cpu, steps4=3, steps5=1):
     return out
 
 
+def shard_inputs(rank, B):
+    """Rank r's config-2 shard: systems [r B, (r+1) B) of the rank-invariant
+    seeded stream (workloads.lcp_batch draws system b from its own seed)."""
+    from paper_2008_03276_b200.workloads import lcp_batch
+    return lcp_batch(SEED, B, start=rank * B)
+
+
+def make_max_over_ranks(dist, device):
+    """max over ranks of a per-rank float (the device-timed step time):
+    identity with one rank, an all_reduce(MAX) otherwise."""
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return max_over_ranks
+
+
+def headline_config(B):
+    """The config dict of the headline line -- identical in both arms, so
+    the driver can tell they ran the same workload."""
+    return {"workload": "config2: banded LCP batch (4096 systems/GPU), n=1025 (pad 1026), "
+                        "beta=8, paqif_solve_lcp(r=1) semantics",
+            "systems_per_gpu": B, "n": N_ROWS, "beta": BETA, "seed": SEED,
+            "generator": "workloads.lcp_batch(seed, B, start=rank*B)",
+            "l2": "inputs larger than L2 (571 MB/GPU), no flush needed"}
+
+
+def _ref_numba_worker(job):
+    """One host core: the UNMODIFIED reference (baseline/_ref, numba) solving
+    config-2 systems with paqif_solve_lcp(LcpProblem(L, f), r=1) for about
+    `secs` after a JIT warm-up."""
+    lo, hi, secs = job
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    from paqif.bandcore import BandedMatrix
+    from paqif.lcp import LcpProblem
+    from paqif.parallel import paqif_solve_lcp
+    from paper_2008_03276_b200.workloads import lcp_batch
+    bands, f = lcp_batch(SEED, hi - lo, start=lo)
+    solve = lambda b: paqif_solve_lcp(LcpProblem(BandedMatrix(N_PAD, BETA, bands[b]), f[b]), 1)
+    solve(0)  # JIT compile / cache load
+    t0 = time.perf_counter()
+    k = 0
+    while k < 1 or (time.perf_counter() - t0 < secs and k < hi - lo):
+        solve(k)
+        k += 1
+    return k, time.perf_counter() - t0
+
+
+def reference_code_rate(threads, secs=6.0):
+    """Config 2 through the reference's own code (baseline/_ref, numba),
+    one process per host core on its own slice of the batch.  None when
+    baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "paqif")):
+        return None
+    import multiprocessing as mp
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
+        os.environ[v] = "1"
+    os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="numba_"))
+    per = 256
+    jobs = [(w * per, (w + 1) * per, secs) for w in range(threads)]
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(threads) as pool:
+        res = pool.map(_ref_numba_worker, jobs)
+    wall = time.perf_counter() - t0
+    solved = sum(k for k, _ in res)
+    busy = max(t for _, t in res)
+    return {"value": solved * N_ROWS / busy, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{solved} config-2 systems through baseline/_ref paqif_solve_lcp(r=1) "
+                      f"(numba), {threads} processes x ~{secs:.0f} s ({wall:.1f} s wall incl. "
+                      f"JIT warm-up)"}
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N > 1 with no launcher: run this script under
+    torch.distributed.run, one rank per GPU, and return its exit code."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU implementation of the path
     (oracle port, all host threads), rank 0 only."""
@@ -360,13 +508,16 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, workloads.lcp_batch)",
-        "config": {"workload": "config2: banded LCP batch, n=1025 (pad 1026), beta=8",
-                   "systems_per_step": sample, "seed": SEED},
+        "config": headline_config(sample),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} config-2 systems per step (oracle/paqif_oracle.c "
                                    f"restating paqif_solve_lcp r=1), {threads} host threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    # beside the port: the reference's own numba code path on the same cores
+    ref_code = None if args.no_ref_code else reference_code_rate(threads)
+    if ref_code is not None:
+        line["reference_code"] = ref_code
     print(json.dumps(line), flush=True)
 
 
@@ -383,12 +534,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ehl", action="store_true", help="skip the config-1/3/4/5 EHL lines")
     ap.add_argument("--no-point", action="store_true", help="skip the config-4/5 point lines")
+    ap.add_argument("--no-ref-code", action="store_true",
+                    help="reference arm: skip timing the reference's numba code (baseline/_ref)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        raise SystemExit(relaunch_distributed(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -403,11 +560,10 @@ def main():
 
     from paper_2008_03276_b200 import _native
     from paper_2008_03276_b200.batch import LcpSolver
-    from paper_2008_03276_b200.workloads import lcp_batch
 
     B = args.batch
     exact = args.exact
-    bands_h, f_h = lcp_batch(SEED, B, start=rank * B)
+    bands_h, f_h = shard_inputs(rank, B)
     # pinned host copies: the e2e path reads these every step
     bands_pin = torch.from_numpy(bands_h).pin_memory()
     f_pin = torch.from_numpy(f_h).pin_memory()
@@ -422,12 +578,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    max_over_ranks = make_max_over_ranks(dist, "cuda")
 
     for _ in range(args.warmup):
         solver.launch(bands, f)
@@ -515,13 +666,11 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded per system, workloads.lcp_batch; inputs 571 MB/GPU > L2, "
                 "no flush needed)",
-        "config": {"workload": "config2: 4096 banded LCPs/GPU, n=1025 (pad 1026), beta=8, "
-                               "paqif_solve_lcp(r=1) semantics",
-                   "systems_per_gpu": B, "n": N_ROWS, "beta": BETA, "seed": SEED,
-                   "arith": "exact (reference rounding, bit-exact vs oracle)" if exact
-                   else "fma (within 1e-9 of exact; same passes and active sets, see "
-                        "other_arith.parity_fma_vs_exact)", "mean_passes": float(np.mean(passes)),
-                   "l2": "inputs larger than L2"},
+        "config": headline_config(B),
+        "arith": "exact (reference rounding, bit-exact vs oracle)" if exact
+                 else "fma (within 1e-9 of exact; same passes and active sets, see "
+                      "other_arith.parity_fma_vs_exact)",
+        "mean_passes": float(np.mean(passes)),
         "gpu_launches": args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
@@ -541,6 +690,7 @@ def main():
     if not args.no_ehl:
         line["secondary"] = ehl_secondary(rank, world, with_cpu=(rank == 0 and world == 1
                                                                   and not args.no_cpu_baseline),
+                                          max_over_ranks=max_over_ranks, barrier=barrier,
                                           point_steps=(0, 0) if args.no_point else (3, 1))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()

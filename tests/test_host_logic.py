@@ -201,44 +201,75 @@ def _free_port():
 
 
 def _shard_worker(rank, world, port, q):
+    """One rank of bench.py's sharded configs, over gloo: its config-2 shard
+    (bench.shard_inputs), its config-3 cases (bench.config3_cases) and the
+    max-over-ranks reduction bench.py applies to the step times."""
     import torch.distributed as dist
     import oracle
+    import bench
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     per = 3
-    bands, f = lcp_batch(77, per, n=65, beta=8, start=rank * per)
+    bands, f = bench.shard_inputs(rank, per)
     u, act, passes, res, st = oracle.lcp_batch(bands, f)
+    cases = bench.config3_cases(rank, count=5)
     gathered = [None] * world
-    dist.all_gather_object(gathered, (u, passes))
-    import torch
-    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # bench.py's max-over-ranks timing
+    dist.all_gather_object(gathered, (u, passes, cases))
+    tmax = bench.make_max_over_ranks(dist, "cpu")(float(rank + 1))
     if rank == 0:
-        q.put((gathered, float(t.item())))
+        q.put((gathered, tmax))
     dist.destroy_process_group()
 
 
 def test_weak_scaling_shards_gloo():
     """Two ranks solve disjoint seeded shards with no data-path collective;
-    gathering them reproduces the single-process batch exactly."""
+    gathering them reproduces the single-process batch exactly (config 2),
+    the config-3 case lists tile the single-process list, and the
+    max-over-ranks timing reduction returns the slowest rank's value."""
     import multiprocessing as mp
     import oracle
+    import bench
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    gathered, tmax = q.get(timeout=120)
+    gathered, tmax = q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
     assert tmax == 2.0
-    bands, f = lcp_batch(77, 6, n=65, beta=8)
+    bands, f = bench.shard_inputs(0, 6)
     u, act, passes, res, st = oracle.lcp_batch(bands, f)
     got_u = np.concatenate([g[0] for g in gathered])
     got_p = np.concatenate([g[1] for g in gathered])
     assert np.array_equal(got_u, u) and np.array_equal(got_p, passes)
+    assert gathered[0][2] + gathered[1][2] == bench.config3_cases(0, count=10)
+    assert gathered[0][2] != gathered[1][2]
+
+
+def test_bench_launcher_spawns_ranks():
+    """bench.py --gpus 2 without a launcher re-executes itself under
+    torch.distributed.run; the reference arm prints one line from rank 0
+    with n_gpus = 2 and the same config dict as the GPU arm."""
+    import json
+    import subprocess
+    import sys
+    import bench
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), "--impl",
+                        "reference", "--gpus", "2", "--steps", "1", "--warmup", "3",
+                        "--no-ref-code"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"] == bench.headline_config(bench.B_PER_GPU)
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
 
 
 class TestTvdHost:
