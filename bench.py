@@ -275,12 +275,18 @@ def ehl_secondary(rank, world, with_cpu, max_over_ranks, barrier, steps1=200, st
     info = b3.info.cpu().numpy()
     ms3f = timed(LineContactBatch([_line_params(m, l) for m, l in cases], 1024, exact=False),
                  steps3)
+    # the fused one-CTA-per-case kernel on the same batch, for comparison
+    ms3_fused = timed(LineContactBatch([_line_params(m, l) for m, l in cases], 1024,
+                                       path="fused"), steps3)
     fl3 = config3_flops()
     tf3 = len(cases) * fl3 / (ms3 * 1e-3) / 1e12
     tf3f = len(cases) * fl3 / (ms3f * 1e-3) / 1e12
     out["config3"] = {"metric": "EHL line-contact case-iterations/s (1024 cases/GPU, N=1025)",
                       "value": world * len(cases) * 1e3 / ms3, "unit": "case-iters/s",
                       "ms_per_iter": ms3, "scaling": "weak", "n_gpus": world,
+                      "path": "split (phase A / batched rung solves / phase C)",
+                      "fused_path_ms_per_iter": ms3_fused,
+                      "gpu_launches_per_iter": 3,
                       "ladder_cases_last_iter": int(np.sum((info & 3) > 0)),
                       "roofline": {"bound": "fp64", "achieved": tf3,
                                    "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",

@@ -57,6 +57,11 @@ extern "C" {
 
 /* flags */
 #define PAQIF_FLAG_EXACT 1u /* reference rounding: no FMA, IEEE division (bit-exact kernels) */
+/* EHL line steps (paqif_ehl.h): the path for a batch of cases.  Default:
+ * the fused one-CTA-per-case kernel below 2 x SM-count cases, the split
+ * three-kernel path (phase A / batched rung solves / phase C) from there. */
+#define PAQIF_FLAG_LINE_SPLIT 2u /* force the split path */
+#define PAQIF_FLAG_LINE_FUSED 4u /* force the fused path */
 
 /* library identity / diagnostics */
 const char *paqif_version(void);

@@ -16,6 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "libpaqif_b200.so")
 
 FLAG_EXACT = 1
+FLAG_LINE_SPLIT = 2   # EHL line steps: force the split three-kernel path
+FLAG_LINE_FUSED = 4   # EHL line steps: force the fused one-CTA-per-case kernel
 
 LCP_OK = 0
 LCP_FACTOR_BREAKDOWN = 1

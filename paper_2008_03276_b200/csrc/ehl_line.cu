@@ -23,7 +23,10 @@
 // convolution and the load sum use a different summation order than
 // numpy's BLAS dot / pairwise sum (documented tolerance).
 #include <cfloat>
+#include <cstdlib>
 #include "aqif2.cuh"
+#include "aqif_warp.cuh"
+#include "zsolve.cuh"
 #include "ehl_common.cuh"
 #include "capi_util.cuh"
 
@@ -209,74 +212,33 @@ __device__ void line_drive_update(paqif_ehl_line_drive& d, double res, int fb, d
   if (d.outer >= d.max_outer) d.done = 3;
 }
 
-#ifdef PAQIF_LINE_PROF  // dev: phase cycles of case 0, printed per launch
-#define LINE_T(i) lt##i = clock64()
-#else
-#define LINE_T(i)
-#endif
 
-// One outer iteration of case b; all threads of the CTA call (esm: the
-// CTA's dynamic shared memory).
-template <bool EXACT, bool SMEM>
-__device__ __forceinline__ void line_case(
-    const paqif_ehl_line_cfg& c, int64_t B, const double* __restrict__ table,
-    const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
-    double* h0_io, double* film_out, double* res_out, double* deficit_out, int32_t* info_out,
-    char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv, double* hist_res, double* hist_def,
-    int hist_cap, const int64_t b, double* esm)
-{
-#ifdef PAQIF_LINE_PROF
-  long long lt0 = 0, lt1 = 0, lt2 = 0, lt3 = 0, lt4 = 0, lt5 = 0, lt6 = 0, lt7 = 0;
-#endif
-  int outer = c.outer;
-  if (drv) {  // device-driven solve_ehl: stopped cases skip
-    if (drv[b].done) return;
-    outer = drv[b].outer;
-  }
-  const int n = c.n, N = n + 1, n_int = n - 1;
-  const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
-  const EhlSmemLayout L(n);
-  double* ext = esm + L.ext;
-  double* su = esm + L.su;
-  double* sun = esm + L.sun;
-  double* sfilm = esm + L.film;
-  double* srho = esm + L.rho;
-  double* seps = esm + L.eps;
-  double* sq = esm + L.q;
-  double* sphp = esm + L.php;
-  double* sphm = esm + L.phm;
-  double* sres = esm + L.res;
-  double* ssig = esm + L.sig;
-  double* sdef = esm + L.def;
-  double* red = esm + L.red;
-  // line system: shared memory, or this case's workspace for large n
-  double* wsd = reinterpret_cast<double*>(ws + (size_t)b * ws_per_case);
-  double* band = SMEM ? esm + L.band : wsd;  // SMEM: shared address space known
-  double* rhs = band + aqif2_band_doubles(n_sys);
-  double* rec = rhs + aqif2_rhs_doubles(n_sys);
-  aqif2_zero_pads(band, rhs, n_sys);
-  double* xsol = band;  // x overwrites the band after the factor
-  const double ph = p_hertz[b], lam = lamv[b];
+// ------------------------------------------------------------------ phases
+// The outer iteration of one case in three phases, shared by the fused
+// kernel (one CTA per case runs all three, the solve on one warp) and the
+// split path for large batches (phase A, a batched solve of every case's
+// rung systems, phase C as three kernels).
+
+// Phase A: film, rheology, limited faces and Reynolds residual of the
+// current pressure su (solver.py:141-149); fills sdef, sfilm, srho, seps,
+// sq, sphp, sphm, sres.  All threads call.
+__device__ __forceinline__ void line_phase_a(const paqif_ehl_line_cfg& c, double h0, double ph,
+                                             double lam, const double* su, const double* ext,
+                                             double* sdef, double* sfilm, double* srho,
+                                             double* seps, double* sq, double* sphp,
+                                             double* sphm, double* sres, double* red) {
+  const int n = c.n, N = n + 1;
   const double h = c.h;
   const double sign = -1.0 / 3.141592653589793;
-  double h0 = h0_io[b];
-
-  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
-  ext4_build(table, n, ext);
-  __syncthreads();
-
-  LINE_T(0);
-  // ---- film, rheology, faces, residual of the current pressure
   toeplitz_conv(su, ext, n, 1.0, sdef);
   __syncthreads();
-  LINE_T(1);
   double qmax = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     const double x = c.lo + h * (double)i;
     const double fv = (h0 + 0.5 * (x * x)) + sign * sdef[i];
     double rho, eps;
     rheology(su[i], fv, c, ph, lam, rho, eps);
-    sfilm[i] = fv;
+    if (sfilm) sfilm[i] = fv;
     srho[i] = rho;
     seps[i] = eps;
     sq[i] = rho * fv;
@@ -299,70 +261,75 @@ __device__ __forceinline__ void line_case(
     sres[i] = (e_p * (su[i + 1] - su[i]) + e_m * (su[i - 1] - su[i])) / h - fd;
   }
   __syncthreads();
+}
 
-  LINE_T(2);
-  // kernel sensitivities (film.sensitivity, sweeps.kernel_nu)
-  const double s0 = sign * table[0], s1 = sign * table[1], s2 = sign * table[2];
-  const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
-                                   : (2.0 - c.kappa) / 2.0 + (1.0 - c.kappa) / 4.0;
-  const double ks0n = s0, ks1n = s1;
-  const double ks0w = nu * (s0 - 0.25 * (2.0 * s1 + 0.0));
-  const double ks1w = nu * (s1 - 0.25 * (s0 + s2 + 0.0));
+// kernel sensitivities of the plain (Newton) and weighted rows
+// (film.sensitivity, sweeps.kernel_nu)
+struct LineKs {
+  double ks0n, ks1n, ks0w, ks1w;
+  __device__ LineKs(const paqif_ehl_line_cfg& c, const double* table) {
+    const double sign = -1.0 / 3.141592653589793;
+    const double s0 = sign * table[0], s1 = sign * table[1], s2 = sign * table[2];
+    const double nu = c.variant == 0 ? (2.0 - c.kappa) / 2.0
+                                     : (2.0 - c.kappa) / 2.0 + (1.0 - c.kappa) / 4.0;
+    ks0n = s0;
+    ks1n = s1;
+    ks0w = nu * (s0 - 0.25 * (2.0 * s1 + 0.0));
+    ks1w = nu * (s1 - 0.25 * (s0 + s2 + 0.0));
+  }
+};
 
-  // rung -1: combined (per-row Ls1/Ls4); 0..2: Ls4 with scheme/first-order/diagonal
-  int rung = -1;
-  int st = 1;
-  int weighted_rows = 0;
-  for (; rung <= 2; ++rung) {
-    int wcount = 0;
-    for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
-      double e[5] = {0.0, 0.0, 1.0, 0.0, 0.0};
-      double rr = 0.0;
-      if (r < n_int) {
-        const int i = r + 1;
-        const bool wrow = (seps[i] / h) <= kSwitch;
-        wcount += wrow;
-        const bool weighted = rung >= 0 || wrow;
-        assemble_row(i, srho, seps, sphp, sphm, h, weighted, rung < 0 ? 0 : rung,
-                     weighted ? ks0w : ks0n, weighted ? ks1w : ks1n, e);
-        rr = sres[i];
-      }
+// Assemble rung `rung` of row r of the padded change system (rung -1: the
+// combined per-row Ls1/Ls4 system; 0..2: Ls4 with scheme / first-order /
+// diagonal Jacobian, solver.py:153-168, sweeps.py:276-295).  Writes the 5
+// band entries (offsets -2..2, exact zeros outside the padded matrix) and
+// returns the right side; *wrow = the row is weighted (eps/h <= 0.6).
+__device__ __forceinline__ double line_row(const paqif_ehl_line_cfg& c, int rung, int r,
+                                           int n_int, int n_sys, const double* srho,
+                                           const double* seps, const double* sphp,
+                                           const double* sphm, const double* sres,
+                                           const LineKs& ks, double* e, bool* wrow) {
+  const double h = c.h;
+  e[0] = 0.0; e[1] = 0.0; e[2] = 1.0; e[3] = 0.0; e[4] = 0.0;
+  double rr = 0.0;
+  *wrow = false;
+  if (r < n_int) {
+    const int i = r + 1;
+    *wrow = (seps[i] / h) <= kSwitch;
+    const bool weighted = rung >= 0 || *wrow;
+    assemble_row(i, srho, seps, sphp, sphm, h, weighted, rung < 0 ? 0 : rung,
+                 weighted ? ks.ks0w : ks.ks0n, weighted ? ks.ks1w : ks.ks1n, e);
+    rr = sres[i];
+  }
 #pragma unroll
-      for (int d = 0; d < 5; ++d) {
-        const int col = r + d - kEhlBeta;
-        // padded-matrix semantics: rows beyond n_int are identity; entries
-        // leaving the (padded) matrix are exact zeros
-        const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (d == kEhlBeta);
-        band2_ref(band, n_sys, r, d - kEhlBeta) = keep ? e[d] : 0.0;
-      }
-      rhs[kBandPad + r] = rr;
-    }
-    if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
-    __syncthreads();
-    LINE_T(3);
-    // solve on warp 0 (aqif2: factor + fused W, Z outside-in)
-    int* flag = reinterpret_cast<int*>(red + 30);
-    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, xsol, flag) & 1;
-    if (!st) break;
+  for (int d = 0; d < 5; ++d) {
+    const int col = r + d - kEhlBeta;
+    // padded-matrix semantics: rows beyond n_int are identity; entries
+    // leaving the (padded) matrix are exact zeros
+    const bool keep = r < n_int ? (col >= 0 && col < n_sys) : (d == kEhlBeta);
+    if (!keep) e[d] = 0.0;
   }
-  if (st) {
-    // every rung broke down: the reference re-raises (robust_line_solve)
-    if (threadIdx.x == 0) {
-      res_out[b] = __longlong_as_double(0x7ff8000000000000ll);
-      if (deficit_out) deficit_out[b] = __longlong_as_double(0x7ff8000000000000ll);
-      info_out[b] = 1 << 8;
-      if (drv) drv[b].done = 4;
-    }
-    return;
-  }
+  return rr;
+}
 
-  LINE_T(4);
-  // ---- update (solver.py:169-181)
+// Phase C: clip, weighted spread and update (solver.py:169-181), deformation
+// of the new pressure, force balance, complementarity residual and the
+// outputs / drive bookkeeping of case b.  xsol(i) = the line solve's change
+// of unknown i; seps holds phase A's eps (the weighted mask) on entry.
+template <class XS>
+__device__ __forceinline__ void line_phase_c(
+    const paqif_ehl_line_cfg& c, int outer, double h0, double ph, double lam, XS xsol,
+    const double* su, double* sun, double* ssig, const double* ext, double* sdef, double* sfilm,
+    double* seps, double* sq, double* red, int rung, int weighted_rows, double* u_io,
+    double* h0_io, double* film_out, double* res_out, double* deficit_out, int32_t* info_out,
+    paqif_ehl_line_drive* drv, double* hist_res, double* hist_def, int hist_cap, int64_t b) {
+  const int n = c.n, N = n + 1;
+  const double h = c.h;
   bool finite = true;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     double sg = 0.0;
     if (i >= 1 && i <= n - 1) {
-      sg = xsol[i - 1];
+      sg = xsol(i - 1);
       finite &= isfinite(sg);
       sg = np_minimum(np_maximum(sg, -c.max_change), c.max_change);
     }
@@ -379,11 +346,9 @@ __device__ __forceinline__ void line_case(
     sun[i] = (i == 0 || i == n) ? 0.0 : np_maximum(0.0, v);
   }
   const int fin_all = __syncthreads_and(finite);
-  LINE_T(5);
   // ---- deformation of the new pressure, force balance, residual
   toeplitz_conv(sun, ext, n, 1.0, sdef);
   __syncthreads();
-  LINE_T(6);
   int fb = 0;
   double deficit_v = __longlong_as_double(0x7ff8000000000000ll);
   if ((outer + 1) % c.force_every == 0) {
@@ -411,13 +376,89 @@ __device__ __forceinline__ void line_case(
     if (drv) line_drive_update(drv[b], cmax / h, fb, deficit_v, fin_all, hist_res, hist_def,
                                hist_cap, b);
   }
-#ifdef PAQIF_LINE_PROF
-  LINE_T(7);
-  if (b == 0 && threadIdx.x == 0)
-    printf("[line_prof] n=%d conv1 %lld rheo/faces %lld assemble %lld solve(last rung) %lld update %lld conv2 %lld resid %lld rung %d\n",
-           n, lt1 - lt0, lt2 - lt1, lt3 - lt2, lt4 - lt3, lt5 - lt4, lt6 - lt5, lt7 - lt6, rung);
+}
 
-#endif
+// every rung broke down: the reference re-raises (robust_line_solve)
+__device__ __forceinline__ void line_all_rungs_failed(int64_t b, double* res_out,
+                                                      double* deficit_out, int32_t* info_out,
+                                                      paqif_ehl_line_drive* drv) {
+  if (threadIdx.x == 0) {
+    res_out[b] = __longlong_as_double(0x7ff8000000000000ll);
+    if (deficit_out) deficit_out[b] = __longlong_as_double(0x7ff8000000000000ll);
+    info_out[b] = 1 << 8;
+    if (drv) drv[b].done = 4;
+  }
+}
+
+// One outer iteration of case b, fused; all threads of the CTA call (esm:
+// the CTA's dynamic shared memory).
+template <bool EXACT, bool SMEM>
+__device__ __forceinline__ void line_case(
+    const paqif_ehl_line_cfg& c, int64_t B, const double* __restrict__ table,
+    const double* __restrict__ p_hertz, const double* __restrict__ lamv, double* u_io,
+    double* h0_io, double* film_out, double* res_out, double* deficit_out, int32_t* info_out,
+    char* ws, size_t ws_per_case, paqif_ehl_line_drive* drv, double* hist_res, double* hist_def,
+    int hist_cap, const int64_t b, double* esm)
+{
+  int outer = c.outer;
+  if (drv) {  // device-driven solve_ehl: stopped cases skip
+    if (drv[b].done) return;
+    outer = drv[b].outer;
+  }
+  const int n = c.n, N = n + 1, n_int = n - 1;
+  const int n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+  const EhlSmemLayout L(n);
+  double* ext = esm + L.ext;
+  double* su = esm + L.su;
+  double* red = esm + L.red;
+  // line system: shared memory, or this case's workspace for large n
+  double* wsd = reinterpret_cast<double*>(ws + (size_t)b * ws_per_case);
+  double* band = SMEM ? esm + L.band : wsd;  // SMEM: shared address space known
+  double* rhs = band + aqif2_band_doubles(n_sys);
+  double* rec = rhs + aqif2_rhs_doubles(n_sys);
+  aqif2_zero_pads(band, rhs, n_sys);
+  double* xsol = band;  // x overwrites the band after the factor
+  const double ph = p_hertz[b], lam = lamv[b];
+  const double h0 = h0_io[b];
+
+  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
+  ext4_build(table, n, ext);
+  __syncthreads();
+  line_phase_a(c, h0, ph, lam, su, ext, esm + L.def, esm + L.film, esm + L.rho, esm + L.eps,
+               esm + L.q, esm + L.php, esm + L.phm, esm + L.res, red);
+  const LineKs ks(c, table);
+
+  // rung -1: combined (per-row Ls1/Ls4); 0..2: Ls4 with scheme/first-order/diagonal
+  int rung = -1;
+  int st = 1;
+  int weighted_rows = 0;
+  for (; rung <= 2; ++rung) {
+    int wcount = 0;
+    for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
+      double e[5];
+      bool wrow;
+      const double rr = line_row(c, rung, r, n_int, n_sys, esm + L.rho, esm + L.eps,
+                                 esm + L.php, esm + L.phm, esm + L.res, ks, e, &wrow);
+      wcount += wrow;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) band2_ref(band, n_sys, r, d - kEhlBeta) = e[d];
+      rhs[kBandPad + r] = rr;
+    }
+    if (rung < 0) weighted_rows = (int)block_sum((double)wcount, red);
+    __syncthreads();
+    // solve on warp 0 (aqif2: factor + fused W, Z outside-in)
+    int* flag = reinterpret_cast<int*>(red + 30);
+    st = aqif2_solve<EXACT>(band, rhs, n_sys, rec, xsol, flag) & 1;
+    if (!st) break;
+  }
+  if (st) {
+    line_all_rungs_failed(b, res_out, deficit_out, info_out, drv);
+    return;
+  }
+  line_phase_c(c, outer, h0, ph, lam, [&](int i) { return xsol[i]; }, su, esm + L.sun,
+               esm + L.sig, ext, esm + L.def, esm + L.film, esm + L.eps, esm + L.q, red, rung,
+               weighted_rows, u_io, h0_io, film_out, res_out, deficit_out, info_out, drv,
+               hist_res, hist_def, hist_cap, b);
 }
 
 // Grid = one CTA per SM pulling cases from a queue (`queue` non-null: the
@@ -469,6 +510,237 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
 #endif
 }
 
+// ------------------------------------------------------------- split path
+// Large batches (config 3): the fused kernel runs one case per SM with the
+// level chain of its line solve on one warp while seven wait.  The split
+// path runs the outer iteration as three kernels:
+//   A  one CTA per case: phase A and the four rung systems of the case
+//      (combined, Ls4 scheme / first-order / diagonal) into its workspace
+//   S  every rung system of every case solved side by side by the
+//      throughput engine (aqif_warp.cuh: 4 lanes per system, 8 per warp,
+//      band streamed from L2 by cp.async hooks, pivot records to a Z
+//      stack, full outside-in Z solve): the reference's ladder tries the
+//      rungs in order; solving them all at once costs no extra chain
+//   C  one CTA per case: the first rung that did not break down, then
+//      phase C.
+// Same arithmetic as the fused path per phase (the general engine is
+// bit-identical to aqif2 in exact mode, tools/aqif2_check.cu).
+constexpr int kRungs = 4;
+
+struct SplitLayout {  // per-case workspace, offsets in doubles
+  int n_sys, s;
+  size_t band, rhs, x, zs, eps, ints, total;
+  __host__ __device__ explicit SplitLayout(int n) {
+    const int n_int = n - 1;
+    n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+    s = n_sys / 2;
+    size_t o = 0;
+    band = o; o += (size_t)kRungs * 5 * n_sys;
+    rhs = o; o += n_sys;
+    x = o; o += (size_t)kRungs * n_sys;
+    zs = o; o += (size_t)kRungs * (s + 1) * PivotLayout<2>::kSize;
+    eps = o; o += (size_t)n + 1;
+    o = (o + 1) & ~(size_t)1;
+    ints = o; o += 4;  // status[kRungs] (int32), weighted rows (int32)
+    total = (o + 31) & ~(size_t)31;
+  }
+};
+
+struct SplitSmemA {  // phase-A kernel, offsets in doubles
+  int ext, su, def, rho, eps, q, php, phm, res, red, total;
+  __host__ __device__ explicit SplitSmemA(int n) {
+    const int NA = (n + 1 + 3 + 1) & ~1;
+    int o = 0;
+    ext = o; o += ext4_doubles(n); o = (o + 1) & ~1;
+    su = o; o += NA; def = o; o += NA; rho = o; o += NA; eps = o; o += NA; q = o; o += NA;
+    php = o; o += NA; phm = o; o += NA; res = o; o += NA; red = o; o += 32;
+    total = o;
+  }
+};
+
+struct SplitSmemC {  // phase-C kernel
+  int ext, su, sun, sig, def, film, eps, q, red, total;
+  __host__ __device__ explicit SplitSmemC(int n) {
+    const int NA = (n + 1 + 3 + 1) & ~1;
+    int o = 0;
+    ext = o; o += ext4_doubles(n); o = (o + 1) & ~1;
+    su = o; o += NA; sun = o; o += NA; sig = o; o += NA; def = o; o += NA; film = o; o += NA;
+    eps = o; o += NA; q = o; o += NA; red = o; o += 32;
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(kEhlThreads)
+line_split_a_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
+                    const double* __restrict__ p_hertz, const double* __restrict__ lamv,
+                    const double* __restrict__ u_io, const double* __restrict__ h0_io, double* ws,
+                    size_t ws_per_case, const paqif_ehl_line_drive* drv)
+{
+  extern __shared__ __align__(16) double esm[];
+  const int64_t b = blockIdx.x;
+  if (b >= B || (drv && drv[b].done)) return;
+  const int n = c.n, N = n + 1, n_int = n - 1;
+  const SplitSmemA L(n);
+  const SplitLayout W(n);
+  const int n_sys = W.n_sys;
+  double* w = ws + (size_t)b * ws_per_case;
+  double* su = esm + L.su;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
+  ext4_build(table, n, esm + L.ext);
+  __syncthreads();
+  line_phase_a(c, h0_io[b], p_hertz[b], lamv[b], su, esm + L.ext, esm + L.def, nullptr,
+               esm + L.rho, esm + L.eps, esm + L.q, esm + L.php, esm + L.phm, esm + L.res,
+               esm + L.red);
+  const LineKs ks(c, table);
+  int wcount = 0;
+  for (int r = threadIdx.x; r < n_sys; r += blockDim.x) {
+    double rr = 0.0;
+#pragma unroll 1
+    for (int rung = -1; rung <= 2; ++rung) {
+      double e[5];
+      bool wrow;
+      rr = line_row(c, rung, r, n_int, n_sys, esm + L.rho, esm + L.eps, esm + L.php,
+                    esm + L.phm, esm + L.res, ks, e, &wrow);
+      if (rung < 0) wcount += wrow;
+      double* band = w + W.band + (size_t)(rung + 1) * 5 * n_sys;
+#pragma unroll
+      for (int d = 0; d < 5; ++d) band[(size_t)d * n_sys + r] = e[d];
+    }
+    w[W.rhs + r] = rr;
+  }
+  for (int i = threadIdx.x; i < N; i += blockDim.x) w[W.eps + i] = esm[L.eps + i];
+  const int wrows = (int)block_sum((double)wcount, esm + L.red);
+  if (threadIdx.x == 0) reinterpret_cast<int32_t*>(w + W.ints)[kRungs] = wrows;
+}
+
+struct SplitSysPol {
+  static constexpr bool kFuseW = true;
+  static constexpr bool kResidual = false;
+  static constexpr bool kFastDiv = true;        // branch-free divisions, checked repeat
+  static constexpr bool kDivFix = true;         // subnormal midpoints fixed inline
+  static constexpr bool kLazyBreakdown = true;  // breakdown found after the loop
+  static constexpr bool kRecordW = false;
+  using PL = PivotLayout<2>;
+  const double* band;
+  const double* rhs;
+  double* zs;
+  int n;
+  __device__ __forceinline__ const double* raw_ptr(int i, int d) const {
+    return band + (size_t)(d + 2) * n + i;
+  }
+  __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
+  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
+  __device__ __forceinline__ bool pinned(int) const { return false; }
+  __device__ __forceinline__ const double* frhs_ptr(int i) const { return rhs + i; }
+  __device__ __forceinline__ double frhs(int i) const { return rhs[i]; }
+  __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
+    double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
+    const double2* src = reinterpret_cast<const double2*>(pb);
+    for (int idx = gl; idx < PL::kSize / 2; idx += G) dst[idx] = src[idx];
+  }
+  __device__ __forceinline__ void on_w(int, int, double, double) {}
+  __device__ __forceinline__ void on_resid(int, int, double) {}
+  __device__ __forceinline__ const double* record(int k) const {
+    return zs + (size_t)k * PL::kSize;
+  }
+};
+
+constexpr int kSplitWarps = 2;
+constexpr int kSplitPerWarp = 8;  // systems per warp (measured 1/2/4/8: 1.72/1.09/0.99/0.96 ms)
+struct SplitSolveSmem {
+  union {
+    EngineSmem<2> eng;
+    double ring[ZChunk<2>::kRing];
+  };
+};
+
+// Every rung system of every case side by side: system m = case m / kRungs,
+// rung m % kRungs.  The reference tries the rungs in order (combined system,
+// then the Ls4 ladder); solving all four at once costs no extra chain,
+// while a second pass for the cases whose combined system broke down would
+// add a whole level chain (measured: 1.28 vs 0.96 ms per config-3 step).
+// pw systems per warp (groups g >= pw idle); a warp without a live system
+// returns at once.
+template <bool EXACT>
+__global__ void __launch_bounds__(32 * kSplitWarps)
+line_split_solve_kernel(int n, int64_t B, double* ws, size_t ws_per_case,
+                        const paqif_ehl_line_drive* drv, int pw)
+{
+  constexpr int G = Group<2>::G, P = Group<2>::P;
+  __shared__ SplitSolveSmem smem[kSplitWarps * P];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane / G, gl = lane % G;
+  const int64_t m = ((int64_t)blockIdx.x * kSplitWarps + wid) * pw + g;
+  const int64_t b = m / kRungs;
+  const int rung = (int)(m % kRungs);
+  const bool alive = g < pw && m < B * kRungs && !(drv && drv[b < B ? b : 0].done);
+  if (!__any_sync(0xffffffffu, alive)) return;
+  const SplitLayout W(n);
+  const int n_sys = W.n_sys;
+  double* w = ws + (size_t)(alive ? b : 0) * ws_per_case;
+  SplitSysPol pol;
+  pol.band = w + W.band + (size_t)rung * 5 * n_sys;
+  pol.rhs = w + W.rhs;
+  pol.zs = w + W.zs + (size_t)rung * (W.s + 1) * PivotLayout<2>::kSize;
+  pol.n = n_sys;
+  SplitSolveSmem& sm = smem[wid * P + g];
+  int fst = aqif_factor_group<2, EXACT>(pol, n_sys, 1e-14, sm.eng, gl, alive);
+  if (EXACT && __any_sync(0xffffffffu, fst < 0)) {
+    // a quotient left the branch-free division's range: repeat with IEEE
+    // divisions (the other systems of the warp idle)
+    __syncwarp();
+    const int f2 = aqif_factor_group<2, EXACT, SplitSysPol, false>(pol, n_sys, 1e-14, sm.eng, gl,
+                                                                   alive && fst < 0);
+    if (fst < 0) fst = f2;
+  }
+  __syncwarp();
+  double* x = w + W.x + (size_t)rung * n_sys;
+  const int zst = zsolve_group<2, EXACT, true>(pol.zs, n_sys, x, sm.ring, gl, alive && fst == 0);
+  if (alive && gl == 0)
+    reinterpret_cast<int32_t*>(w + W.ints)[rung] = (fst || zst) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kEhlThreads)
+line_split_c_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
+                    const double* __restrict__ p_hertz, const double* __restrict__ lamv,
+                    double* u_io, double* h0_io, double* film_out, double* res_out,
+                    double* deficit_out, int32_t* info_out, const double* ws, size_t ws_per_case,
+                    paqif_ehl_line_drive* drv, double* hist_res, double* hist_def, int hist_cap)
+{
+  extern __shared__ __align__(16) double esm[];
+  const int64_t b = blockIdx.x;
+  if (b >= B) return;
+  int outer = c.outer;
+  if (drv) {
+    if (drv[b].done) return;
+    outer = drv[b].outer;
+  }
+  const int n = c.n, N = n + 1;
+  const SplitSmemC L(n);
+  const SplitLayout W(n);
+  const double* w = ws + (size_t)b * ws_per_case;
+  const int32_t* wi = reinterpret_cast<const int32_t*>(w + W.ints);
+  int r = 0;
+  while (r < kRungs && wi[r] != 0) ++r;
+  if (r == kRungs) {
+    line_all_rungs_failed(b, res_out, deficit_out, info_out, drv);
+    return;
+  }
+  const int wrows = wi[kRungs];
+  double* su = esm + L.su;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    su[k] = u_io[b * N + k];
+    esm[L.eps + k] = w[W.eps + k];
+  }
+  ext4_build(table, n, esm + L.ext);
+  __syncthreads();
+  const double* xs = w + W.x + (size_t)r * W.n_sys;
+  line_phase_c(c, outer, h0_io[b], p_hertz[b], lamv[b], [&](int i) { return xs[i]; }, su,
+               esm + L.sun, esm + L.sig, esm + L.ext, esm + L.def, esm + L.film, esm + L.eps,
+               esm + L.q, esm + L.red, r - 1, wrows, u_io, h0_io, film_out, res_out,
+               deficit_out, info_out, drv, hist_res, hist_def, hist_cap, b);
+}
+
 }  // namespace paqif
 
 using namespace paqif;
@@ -485,12 +757,19 @@ size_t line_ws_per_case(int64_t n) {
                       (size_t)(s + 1) * kRec2 + 32) * 8;
   return (per + 255) & ~(size_t)255;
 }
+
+size_t split_ws_per_case(int64_t n) {
+  return (size_t)paqif::SplitLayout((int)n).total * 8;
+}
 }  // namespace
 
-// B per-case areas, then the case order (B int32) and the queue counter
+// B per-case areas (the larger of the fused and the split layout), then the
+// case order (B int32) and the queue counter
 extern "C" size_t paqif_ehl_line_workspace_bytes(int64_t B, int64_t n) {
-  if (B < 0 || n < 4) return 0;
-  return (size_t)B * line_ws_per_case(n) + (((size_t)B * 4 + 4 + 255) & ~(size_t)255);
+  if (B < 0 || n < 4 || n > (1 << 20)) return 0;
+  const size_t per = line_ws_per_case(n) > split_ws_per_case(n) ? line_ws_per_case(n)
+                                                                 : split_ws_per_case(n);
+  return (size_t)B * per + (((size_t)B * 4 + 4 + 255) & ~(size_t)255);
 }
 
 namespace paqif {
@@ -530,7 +809,8 @@ int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const d
   const EhlSmemLayout L(cfg->n);
   const size_t smem = (size_t)L.total * 8;
   if (smem > 227 * 1024) return set_arg_error("ehl_line: grid too fine for one CTA");
-  const size_t per = line_ws_per_case(cfg->n);
+  const size_t per = line_ws_per_case(cfg->n) > split_ws_per_case(cfg->n)
+                         ? line_ws_per_case(cfg->n) : split_ws_per_case(cfg->n);
   int32_t* order = reinterpret_cast<int32_t*>((char*)workspace + (size_t)B * per);
   int* queue = reinterpret_cast<int*>(order + B);
   static int sms = 0;
@@ -539,8 +819,40 @@ int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const d
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool queued = B > sms;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool split = (flags & PAQIF_FLAG_LINE_SPLIT) ||
+                     (!(flags & PAQIF_FLAG_LINE_FUSED) && B >= 2 * (int64_t)sms);
+  if (split) {
+    const bool exact = flags & PAQIF_FLAG_EXACT;
+    const size_t sa = (size_t)SplitSmemA(cfg->n).total * 8, sc = (size_t)SplitSmemC(cfg->n).total * 8;
+    cudaFuncSetAttribute(line_split_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
+    cudaFuncSetAttribute(line_split_c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+    static int pw = 0;
+    if (!pw) {
+      const char* e = getenv("PAQIF_SPLIT_PW");  // dev knob: systems per warp
+      pw = e ? atoi(e) : kSplitPerWarp;
+      if (pw < 1 || pw > Group<2>::P) pw = kSplitPerWarp;
+    }
+    const int64_t warps = (B * kRungs + pw - 1) / pw;
+    const unsigned sgrid = (unsigned)((warps + kSplitWarps - 1) / kSplitWarps);
+    double* wsd = reinterpret_cast<double*>(workspace);
+    const size_t perd = per / 8;
+    for (int32_t s = 0; s < steps; ++s) {
+      line_split_a_kernel<<<(unsigned)B, kEhlThreads, sa, st>>>(*cfg, B, table, p_hertz, lam, u,
+                                                                 h0, wsd, perd, drv);
+      if (exact)
+        line_split_solve_kernel<true><<<sgrid, 32 * kSplitWarps, 0, st>>>(cfg->n, B, wsd, perd,
+                                                                            drv, pw);
+      else
+        line_split_solve_kernel<false><<<sgrid, 32 * kSplitWarps, 0, st>>>(cfg->n, B, wsd, perd,
+                                                                             drv, pw);
+      line_split_c_kernel<<<(unsigned)B, kEhlThreads, sc, st>>>(
+          *cfg, B, table, p_hertz, lam, u, h0, film, res, deficit, info, wsd, perd, drv, hist_res,
+          hist_def, hist_cap);
+    }
+    return check_launch(who);
+  }
+  const bool queued = B > sms;
   auto kern = (flags & PAQIF_FLAG_EXACT)
                   ? (L.sys_in_smem ? ehl_line_kernel<true, true> : ehl_line_kernel<true, false>)
                   : (L.sys_in_smem ? ehl_line_kernel<false, true> : ehl_line_kernel<false, false>);

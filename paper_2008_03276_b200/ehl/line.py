@@ -2,8 +2,11 @@
 
 ``LineContactBatch`` keeps B independent line contacts (same grid, per-case
 load numbers) resident in HBM and advances all of them by one outer
-iteration of solve_ehl per ``step()`` -- one fused kernel launch
-(csrc/ehl_line.cu, C ABI include/paqif_ehl.h).
+iteration of solve_ehl per ``step()`` (csrc/ehl_line.cu, C ABI
+include/paqif_ehl.h): one fused kernel launch (one CTA per case) for small
+batches, or, from 2 x SM-count cases on (config 3), the split path -- phase
+A per case, every case's ladder-rung systems solved side by side by the
+throughput AQIF engine, phase C per case.  ``path`` forces either.
 """
 
 from __future__ import annotations
@@ -79,10 +82,13 @@ class LineContactBatch:
 
     def __init__(self, params_list, intervals: int, scheme: str = "Lhs1",
                  kappa: float = 1 / 3, limiter: str = "kappa", omega: float | None = None,
-                 force_every: int = 5, exact: bool = True, u0=None, h0=None):
+                 force_every: int = 5, exact: bool = True, u0=None, h0=None,
+                 path: str = "auto"):
         torch = _native.torch_cuda()
         self.L = _bind(_native.lib())
         params_list = list(params_list)
+        if path not in ("auto", "split", "fused"):
+            raise ContractViolationError(f"unknown path {path!r}")
         if not params_list:
             raise ContractViolationError("empty batch")
         p = params_list[0]
@@ -110,7 +116,8 @@ class LineContactBatch:
                            omega=p.omega if omega is None else omega, max_change=p.max_change,
                            relax_c=p.relax_c, max_h0_step=p.max_h0_step,
                            load_target=p.load_target, alpha=p.alpha, z=p.z, p0=p.p0)
-        self.flags = _native.FLAG_EXACT if exact else 0
+        self.flags = (_native.FLAG_EXACT if exact else 0) | {
+            "auto": 0, "split": _native.FLAG_LINE_SPLIT, "fused": _native.FLAG_LINE_FUSED}[path]
         dev = "cuda"
         N = self.n + 1
         self.table = torch.from_numpy(kernel_line(self.n, self.h).table).to(dev)
