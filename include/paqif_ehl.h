@@ -184,6 +184,20 @@ int paqif_ehl_point_set_state(paqif_ehl_point *h, const double *u, double h0);
 /* Enqueues one outer iteration (asynchronous on the handle's stream). */
 int paqif_ehl_point_step(paqif_ehl_point *h, int32_t outer, uint32_t flags);
 
+/* Device-side solve_ehl loop for the point contact (ehl/solver.py:210-240):
+ * enqueues `steps` outer iterations; after each, the stop / divergence tests
+ * run on the device against `drive` ([dev], the line contact's record type;
+ * its `outer` is the iteration index and sets the force-balance schedule).
+ * Once the record is done (1 converged, 2 diverging, 3 budget, 4 every rung
+ * of a line solve broke down, 5 non-finite change -- 4/5 stop before the
+ * residual is recorded) every later enqueued kernel returns at once, so the
+ * host synchronises once per chunk.  hist_res / hist_def ([dev], may be
+ * NULL) receive the residual and the load deficit (NaN without a force
+ * balance) of iteration k at k % hist_cap. */
+int paqif_ehl_point_drive_steps(paqif_ehl_point *h, int32_t steps, paqif_ehl_line_drive *drive,
+                                double *hist_res, double *hist_def, int32_t hist_cap,
+                                uint32_t flags);
+
 /* Enqueues one sweep of the public sweep functions on the resident state:
  *   kind 0  _hybrid_x_sweep         (ehl/solver.py:76-128)
  *   kind 1  newton_line_sweep       (ehl/sweeps.py:344-379; immediate updates)

@@ -35,7 +35,12 @@ __host__ __device__ inline size_t pt_sys_doubles(int n_sys) {
   return aqif2_band_doubles(n_sys) + aqif2_rhs_doubles(n_sys) + (size_t)(n_sys / 2 + 1) * kRec2;
 }
 constexpr int kMaxPending = 9;
-enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMSize = 24 };
+enum { kMCount = 0, kMGate = 1, kMAnyW = 2, kMAxis = 3, kMIdx = 12, kMErr = 21, kMStop = 22,
+       kMSize = 24 };
+// meta[kMStop] != 0: a device-driven loop (paqif_ehl_point_drive_steps) has
+// stopped -- every kernel of the later enqueued iterations returns at once
+#define PT_LIVE(meta) \
+  if ((meta)[kMStop]) return
 
 // per-sweep controls (the public sweep variants of sweeps.py / solver.py)
 struct SweepCtl {
@@ -104,6 +109,7 @@ constexpr int kFilmChunk = 128;  // outputs per warp: 32 lanes x 4
 constexpr int kFilmSegMax = 32;  // N <= 4096
 __global__ void __launch_bounds__(32) pt_films_part_kernel(PointDev d, int mode, int first, int L,
                                                            const int32_t* skip) {
+  PT_LIVE(d.meta);
   if (skip && *skip) return;
   const int count = d.meta[kMCount];
   const int p = blockIdx.z;
@@ -172,6 +178,7 @@ __global__ void __launch_bounds__(32 * kPtFilmWarps) pt_films_kernel(PointDev d,
                                                                      size_t rho_off,
                                                                      const int32_t* skip,
                                                                      int nseg) {
+  PT_LIVE(d.meta);
   if (skip && *skip) return;  // the line was solved in a batched run
   const int N = d.N;
   const int count = d.meta[kMCount];
@@ -456,6 +463,7 @@ __device__ void xline_body(PointDev& d, const paqif_ehl_point_cfg& c, const Swee
 template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int j) {
+  PT_LIVE(d.meta);
   if (d.done[j]) return;  // solved inside a batched run of deferred lines
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xline_kernel(PointDev d, paq
 // min(eps)/h test as the line kernel's pass 1, on the run's rheology rows
 // (one block per line).
 __global__ void pt_run_flags_kernel(PointDev d, paqif_ehl_point_cfg c, SweepCtl ctl, int L) {
+  PT_LIVE(d.meta);
   __shared__ double red[32];
   const int l = blockIdx.x;
   if (l >= L) return;
@@ -491,6 +500,7 @@ __global__ void pt_run_flags_kernel(PointDev d, paqif_ehl_point_cfg c, SweepCtl 
 template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kPtThreads, 1) pt_xrun_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                              SweepCtl ctl, int a, int L) {
+  PT_LIVE(d.meta);
   extern __shared__ __align__(16) double xsm[];
   PtShared& S = *reinterpret_cast<PtShared*>(xsm);
   double* sysb = SMEM ? xsm + sizeof(PtShared) / 8
@@ -509,6 +519,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_xrun_kernel(PointDev d, paqi
 
 // deferred weighted changes of the x-sweep (solver.py:115-127)
 __global__ void pt_weighted_kernel(PointDev d, double omega) {
+  PT_LIVE(d.meta);
   if (d.meta[kMAnyW] == 0) return;
   const int N = d.N, n = d.n;
   const size_t total = (size_t)N * N;
@@ -526,13 +537,16 @@ __global__ void pt_weighted_kernel(PointDev d, double omega) {
     d.film_out[g] = v;  // staged: u must not change while neighbours are read
   }
 }
-__global__ void pt_copy_kernel(double* dst, const double* src, size_t count, const int* flag) {
+__global__ void pt_copy_kernel(double* dst, const double* src, size_t count, const int* flag,
+                               const int* meta) {
+  PT_LIVE(meta);
   if (flag && *flag == 0) return;
   for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < count;
        g += (size_t)gridDim.x * blockDim.x)
     dst[g] = src[g];
 }
 __global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
+  PT_LIVE(meta);
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     if (!from_anyw || meta[kMAnyW]) meta[kMGate] = 1;
   }
@@ -542,6 +556,7 @@ __global__ void pt_set_gate_kernel(int* meta, int from_anyw) {
 template <bool EXACT, bool SMEM>
 __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paqif_ehl_point_cfg c,
                                                               SweepCtl ctl, int i) {
+  PT_LIVE(d.meta);
   extern __shared__ __align__(16) double ysm[];
   PtShared& S = *reinterpret_cast<PtShared*>(ysm);
   double* sysb = SMEM ? ysm + sizeof(PtShared) / 8 : d.scratch;
@@ -688,7 +703,12 @@ __global__ void __launch_bounds__(kPtThreads, 1) pt_yline_kernel(PointDev d, paq
 }
 
 // force balance (sweeps.py:521-535, weight h^2)
-__global__ void pt_force_kernel(PointDev d, paqif_ehl_point_cfg c) {
+// drv (device-driven loop): balance only on the reference's schedule,
+// (outer + 1) % force_every == 0 with outer from the drive record
+__global__ void pt_force_kernel(PointDev d, paqif_ehl_point_cfg c,
+                                const paqif_ehl_line_drive* drv) {
+  PT_LIVE(d.meta);
+  if (drv && (drv->outer + 1) % c.force_every != 0) return;
   __shared__ double red[32];
   const size_t total = (size_t)d.N * d.N;
   double part = 0.0;
@@ -705,6 +725,7 @@ __global__ void pt_force_kernel(PointDev d, paqif_ehl_point_cfg c) {
 // reynolds_residual_field (2-D, sweeps.py:124-140) and the complementarity
 // residual; one CTA per row; film_out = h0 + geometry + deformation
 __global__ void pt_residual_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  PT_LIVE(d.meta);
   __shared__ double red[32];
   const int n = d.n, N = d.N;
   const int j = blockIdx.x;
@@ -765,7 +786,63 @@ __global__ void pt_residual_kernel(PointDev d, paqif_ehl_point_cfg c) {
 }
 
 __global__ void pt_finish_kernel(PointDev d, paqif_ehl_point_cfg c) {
+  PT_LIVE(d.meta);
   if (threadIdx.x == 0 && blockIdx.x == 0) d.scal[1] = d.scal[3] / (c.h * c.h);
+}
+
+// zero `words` 4-byte words (the per-sweep resets), unless stopped
+__global__ void pt_zero_kernel(uint32_t* p, size_t words, const int* meta) {
+  PT_LIVE(meta);
+  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < words;
+       g += (size_t)gridDim.x * blockDim.x)
+    p[g] = 0u;
+}
+
+// solve_ehl's per-iteration bookkeeping and stop / divergence tests
+// (ehl/solver.py:219-240, same comparisons in the same order) on the drive
+// record, after the iteration's residual; a stop sets meta[kMStop].
+// A line solve with every rung broken (err bits 0/2) or a non-finite change
+// (bits 1/3) stops before the residual is recorded (the reference raises
+// inside the sweep).
+__global__ void pt_drive_kernel(PointDev d, paqif_ehl_point_cfg c, paqif_ehl_line_drive* drv,
+                                double* hist_res, double* hist_def, int hist_cap) {
+  PT_LIVE(d.meta);
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  paqif_ehl_line_drive& r = *drv;
+  const int err = d.meta[kMErr];
+  if (err & 5) {
+    r.done = 4;
+    d.meta[kMStop] = 1;
+    return;
+  }
+  if (err & 10) {
+    r.done = 5;
+    d.meta[kMStop] = 1;
+    return;
+  }
+  const int k = r.outer;
+  const int fb = (k + 1) % c.force_every == 0;
+  const double res = d.scal[1], deficit = d.scal[2];
+  if (hist_res && hist_cap > 0) {
+    hist_res[k % hist_cap] = res;
+    hist_def[k % hist_cap] = fb ? deficit : __longlong_as_double(0x7ff8000000000000ll);
+  }
+  if (fb) r.deficit = fabs(deficit);
+  r.outer = k + 1;
+  if (res <= r.tol && fabs(r.deficit) <= r.tol_fb) r.done = 1;
+  else if (res < r.best) {
+    r.best = res;
+    r.grow = 0;
+  } else {
+    r.grow += 1;
+    if (r.grow >= 20 && res > 1e3 * fmax(r.best, r.tol)) r.done = 2;
+  }
+  if (!r.done && r.outer >= r.max_outer) r.done = 3;
+  if (r.done) d.meta[kMStop] = 1;
+}
+
+__global__ void pt_drive_begin_kernel(int* meta, const paqif_ehl_line_drive* drv) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) meta[kMStop] = drv->done != 0 ? 1 : 0;
 }
 
 }  // namespace paqif
@@ -788,6 +865,7 @@ struct paqif_ehl_point {
   cudaEvent_t xinfo_ev = nullptr;
   bool xinfo_valid = false;
   bool runs = true;  // PAQIF_PT_RUNS=0 solves every x-line on its own (A/B checks)
+  std::vector<int32_t> pred;  // run-prediction tags for a device-driven chunk
 };
 
 namespace {
@@ -988,14 +1066,18 @@ std::vector<std::pair<int, int>> x_runs(paqif_ehl_point* h, const SweepCtl& ctl)
   std::vector<std::pair<int, int>> runs;
   const int n = h->d.n;
   if (!h->runs) return runs;
+  // tags: the last completed x-sweep's (or, inside a device-driven chunk,
+  // the snapshot taken when the chunk was enqueued)
+  const int32_t* tags = nullptr;
+  if (!h->pred.empty()) tags = h->pred.data();
+  else if (h->xinfo_valid && cudaEventQuery(h->xinfo_ev) == cudaSuccess) tags = h->xinfo_prev;
   if (ctl.defer == 1) {
     runs.emplace_back(1, n);
-  } else if (ctl.defer < 0 && ctl.sel != 0 && h->xinfo_valid &&
-             cudaEventQuery(h->xinfo_ev) == cudaSuccess) {
+  } else if (ctl.defer < 0 && ctl.sel != 0 && tags) {
     constexpr int kMinRun = 4;
     int a = -1;
     for (int j = 1; j <= n; ++j) {
-      const bool dfr = j < n && (h->xinfo_prev[j - 1] & 2) != 0;
+      const bool dfr = j < n && (tags[j - 1] & 2) != 0;
       if (dfr && a < 0) a = j;
       if (!dfr && a >= 0) {
         if (j - a >= kMinRun) runs.emplace_back(a, j);
@@ -1015,9 +1097,9 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   const int n = d.n, N = d.N;
   cudaStream_t st = h->st;
   const size_t NN = (size_t)N * N;
-  cudaMemsetAsync(d.sigma, 0, NN * 8, st);
-  cudaMemsetAsync(&d.meta[kMAnyW], 0, sizeof(int), st);
-  cudaMemsetAsync(d.done, 0, (size_t)N * sizeof(int32_t), st);
+  pt_zero_kernel<<<296, 256, 0, st>>>(reinterpret_cast<uint32_t*>(d.sigma), NN * 2, d.meta);
+  pt_zero_kernel<<<1, 32, 0, st>>>(reinterpret_cast<uint32_t*>(&d.meta[kMAnyW]), 1, d.meta);
+  pt_zero_kernel<<<(N + 255) / 256, 256, 0, st>>>(reinterpret_cast<uint32_t*>(d.done), N, d.meta);
   const auto runs = x_runs(h, ctl);
   size_t next_run = 0;
   const bool certain = ctl.defer == 1;  // every line deferred: no per-line launches needed
@@ -1053,7 +1135,7 @@ void enqueue_x_sweep(paqif_ehl_point* h, const SweepCtl& ctl, bool exact) {
   }
   if (ctl.defer != 0) {
     pt_weighted_kernel<<<296, 256, 0, st>>>(d, ctl.omega);
-    pt_copy_kernel<<<296, 256, 0, st>>>(d.u, d.film_out, NN, &d.meta[kMAnyW]);
+    pt_copy_kernel<<<296, 256, 0, st>>>(d.u, d.film_out, NN, &d.meta[kMAnyW], d.meta);
     pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 1);
     fold(h);
   }
@@ -1090,7 +1172,7 @@ void enqueue_residual(paqif_ehl_point* h) {
   cudaStream_t st = h->st;
   pt_set_gate_kernel<<<1, 32, 0, st>>>(d.meta, 0);
   fold(h);  // film_full: fresh deformation, pending list cleared
-  cudaMemsetAsync(&d.scal[3], 0, sizeof(double), st);
+  pt_zero_kernel<<<1, 32, 0, st>>>(reinterpret_cast<uint32_t*>(&d.scal[3]), 2, d.meta);
   pt_residual_kernel<<<d.N, 256, 0, st>>>(d, h->cfg);
   pt_finish_kernel<<<1, 32, 0, st>>>(d, h->cfg);
 }
@@ -1106,6 +1188,7 @@ extern "C" int paqif_ehl_point_sweep(paqif_ehl_point* h, int32_t kind, int32_t s
   const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
   cudaMemsetAsync(&h->d.meta[kMErr], 0, sizeof(int), h->st);
   cudaMemsetAsync(&h->d.scal[4], 0, sizeof(double), h->st);
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);  // not device-driven
   SweepCtl ctl{sel, kind == 0 ? -1 : (kind == 2 ? 1 : 0), nu_variant, omega};
   if (kind == 3) enqueue_y_sweep(h, ctl, exact);
   else enqueue_x_sweep(h, ctl, exact);
@@ -1114,30 +1197,61 @@ extern "C" int paqif_ehl_point_sweep(paqif_ehl_point* h, int32_t kind, int32_t s
 
 extern "C" int paqif_ehl_point_force_balance(paqif_ehl_point* h) {
   if (!h) return set_arg_error("ehl_point_force_balance");
-  pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, h->cfg);
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
+  pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, h->cfg, nullptr);
   return check_launch("paqif_ehl_point_force_balance");
 }
 
 extern "C" int paqif_ehl_point_residual(paqif_ehl_point* h) {
   if (!h) return set_arg_error("ehl_point_residual");
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
   enqueue_residual(h);
   return check_launch("paqif_ehl_point_residual");
 }
 
+namespace {
+// one outer iteration of solve_ehl (solver.py:205-216): hybrid x-sweep,
+// column sweep, force balance every force_every-th iteration (drv: on the
+// drive record's schedule), complementarity residual
+void enqueue_step(paqif_ehl_point* h, int32_t outer, bool exact, paqif_ehl_line_drive* drv) {
+  const paqif_ehl_point_cfg& c = h->cfg;
+  pt_zero_kernel<<<1, 32, 0, h->st>>>(reinterpret_cast<uint32_t*>(&h->d.meta[kMErr]), 1,
+                                      h->d.meta);
+  pt_zero_kernel<<<1, 32, 0, h->st>>>(reinterpret_cast<uint32_t*>(&h->d.scal[4]), 2, h->d.meta);
+  enqueue_x_sweep(h, SweepCtl{-1, -1, c.variant, c.omega}, exact);
+  enqueue_y_sweep(h, SweepCtl{0, 0, c.variant, c.omega}, exact);
+  if (drv || (outer + 1) % c.force_every == 0)
+    pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, c, drv);
+  enqueue_residual(h);
+}
+}  // namespace
+
 extern "C" int paqif_ehl_point_step(paqif_ehl_point* h, int32_t outer, uint32_t flags) {
   if (!h) return set_arg_error("ehl_point_step");
   prepare_attrs(h);
-  const paqif_ehl_point_cfg& c = h->cfg;
-  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
-  cudaMemsetAsync(&h->d.meta[kMErr], 0, sizeof(int), h->st);
-  cudaMemsetAsync(&h->d.scal[4], 0, sizeof(double), h->st);
-  // solve_ehl (solver.py:205-216): hybrid x-sweep, column sweep, force
-  // balance every force_every-th iteration, complementarity residual
-  enqueue_x_sweep(h, SweepCtl{-1, -1, c.variant, c.omega}, exact);
-  enqueue_y_sweep(h, SweepCtl{0, 0, c.variant, c.omega}, exact);
-  if ((outer + 1) % c.force_every == 0) pt_force_kernel<<<1, 1024, 0, h->st>>>(h->d, c);
-  enqueue_residual(h);
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);  // not device-driven
+  enqueue_step(h, outer, (flags & PAQIF_FLAG_EXACT) != 0, nullptr);
   return check_launch("paqif_ehl_point_step");
+}
+
+extern "C" int paqif_ehl_point_drive_steps(paqif_ehl_point* h, int32_t steps,
+                                           paqif_ehl_line_drive* drive, double* hist_res,
+                                           double* hist_def, int32_t hist_cap, uint32_t flags) {
+  if (!h || !drive || steps < 0 || (hist_res && (!hist_def || hist_cap < 1)))
+    return set_arg_error("ehl_point_drive_steps");
+  prepare_attrs(h);
+  const bool exact = (flags & PAQIF_FLAG_EXACT) != 0;
+  // run prediction for the whole chunk: the last completed x-sweep's tags
+  h->pred.clear();
+  if (h->runs && h->xinfo_valid && cudaEventSynchronize(h->xinfo_ev) == cudaSuccess)
+    h->pred.assign(h->xinfo_prev, h->xinfo_prev + (h->d.n - 1));
+  pt_drive_begin_kernel<<<1, 32, 0, h->st>>>(h->d.meta, drive);
+  for (int32_t s = 0; s < steps; ++s) {
+    enqueue_step(h, 0, exact, drive);
+    pt_drive_kernel<<<1, 32, 0, h->st>>>(h->d, h->cfg, drive, hist_res, hist_def, hist_cap);
+  }
+  h->pred.clear();
+  return check_launch("paqif_ehl_point_drive_steps");
 }
 
 extern "C" int paqif_ehl_point_get(paqif_ehl_point* h, double* u, double* film, double* scal,
@@ -1170,6 +1284,7 @@ extern "C" int paqif_ehl_point_deformation(paqif_ehl_point* h, const double* u, 
   if (!h) return set_arg_error("ehl_point_deformation");
   const size_t NN = (size_t)h->d.N * h->d.N;
   cudaMemcpyAsync(h->d.film_out, u, NN * 8, cudaMemcpyHostToDevice, h->st);
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
   pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
   // deformation_full: fresh base, pending line updates cleared (film.py:67-79)
   fft_deformation(h->plan, h->d.film_out, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount],
@@ -1219,6 +1334,7 @@ extern "C" int paqif_ehl_point_film_lines(paqif_ehl_point* h, int32_t mode, cons
   for (int k = 0; k < L; ++k)
     if (idx[k] < 0 || idx[k] > h->d.n) return set_arg_error("ehl_point_film_lines: index");
   const int N = h->d.N;
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
   cudaMemcpyAsync(&h->d.scal[0], &h0, sizeof(double), cudaMemcpyHostToDevice, h->st);
   for (int k = 0; k < L; ++k) {
     films(h, mode, idx[k], 1, nullptr, h->d.films, h->d.rcache, 4 * (size_t)N);

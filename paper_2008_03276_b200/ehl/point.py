@@ -50,6 +50,8 @@ def _bind(L):
     L.paqif_ehl_point_set_state.restype = ctypes.c_int
     L.paqif_ehl_point_step.argtypes = [vp, i32, u32]
     L.paqif_ehl_point_step.restype = ctypes.c_int
+    L.paqif_ehl_point_drive_steps.argtypes = [vp, i32, vp, vp, vp, i32, u32]
+    L.paqif_ehl_point_drive_steps.restype = ctypes.c_int
     L.paqif_ehl_point_get.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.paqif_ehl_point_get.restype = ctypes.c_int
     L.paqif_ehl_point_stream.argtypes = [vp]
@@ -211,6 +213,39 @@ class PointContact:
         rc = self.L.paqif_ehl_point_step(self._h.ptr, self.outer, self.flags)
         _native.check(rc, "paqif_ehl_point_step")
         self.outer += 1
+
+    def drive_init(self, tol: float, tol_fb: float, max_outer: int, hist_cap: int = 16):
+        """Device solve_ehl record (the line contact's layout, DRIVE_DTYPE):
+        the stop / divergence tests run on the GPU after every iteration."""
+        from .line import DRIVE_DTYPE
+        torch = _native.torch_cuda()
+        rec = np.zeros(1, dtype=DRIVE_DTYPE)
+        rec["tol"], rec["tol_fb"] = tol, tol_fb
+        rec["best"] = rec["deficit"] = np.inf
+        rec["max_outer"], rec["outer"] = max_outer, self.outer
+        self.drive = torch.from_numpy(rec.view(np.uint8)).cuda()
+        self.hist_cap = int(hist_cap)
+        self.hist_res = torch.empty(self.hist_cap, dtype=torch.float64, device="cuda")
+        self.hist_def = torch.empty_like(self.hist_res)
+
+    def drive_steps(self, steps: int) -> None:
+        """Enqueue `steps` device-driven outer iterations (asynchronous on
+        the handle's stream; a stopped record turns the rest into no-ops)."""
+        torch = _native.torch_cuda()
+        torch.cuda.current_stream().synchronize()  # drive buffers written on torch's stream
+        rc = self.L.paqif_ehl_point_drive_steps(self._h.ptr, int(steps), self.drive.data_ptr(),
+                                                self.hist_res.data_ptr(),
+                                                self.hist_def.data_ptr(), self.hist_cap,
+                                                self.flags)
+        _native.check(rc, "paqif_ehl_point_drive_steps")
+
+    def drive_state(self):
+        """Host copy of the drive record (synchronises the handle's stream)."""
+        from .line import DRIVE_DTYPE
+        self.sync()
+        d = self.drive.cpu().numpy().view(DRIVE_DTYPE).copy()[0]
+        self.outer = int(d["outer"])
+        return d
 
     def sweep(self, kind: int, sel: int = -1, nu_variant: int | None = None,
               omega: float | None = None) -> None:

@@ -2,9 +2,12 @@
 
 The line contact runs every outer iteration as ONE fused CUDA launch
 (LineContactBatch with B = 1); the point contact as the native sweep driver
-of csrc/ehl_point.cu (PointContact).  The host only reads back the residual
-and the load deficit for the stop / divergence tests and the ``collect``
-callback, exactly as the reference loop does (solver.py:210-240).
+of csrc/ehl_point.cu (PointContact).  Without a ``collect`` callback the
+whole loop runs on the device for both (drive records: the stop /
+divergence tests of solver.py:219-240 after every iteration, one host
+synchronisation per chunk); with ``collect`` the host steps and reads back
+the residual and the load deficit each iteration, exactly as the reference
+loop does (solver.py:210-240).
 """
 
 from __future__ import annotations
@@ -129,6 +132,46 @@ class _PointDriver:
         snap = self.p.snapshot()
         return snap["u"], snap["h0"]
 
+    def run(self, state, tol, tol_fb, max_outer, chunk=8):
+        """The loop on the device (paqif_ehl_point_drive_steps): one
+        synchronisation per chunk (the first chunk is one iteration, so the
+        next chunks' deferred-run prediction has a finished x-sweep to read);
+        histories replayed into `state` as the host loop appends them."""
+        from ..errors import FactorizationBreakdownError
+        from .line import (DRIVE_BREAKDOWN, DRIVE_CONVERGED, DRIVE_DIVERGING, DRIVE_NONFINITE,
+                           DRIVE_RUNNING)
+        p = self.p
+        p.drive_init(tol, tol_fb, max_outer, hist_cap=chunk)
+        done_before = 0
+        steps = 1
+        while True:
+            p.drive_steps(steps)
+            d = p.drive_state()
+            k = int(d["outer"])
+            hr = p.hist_res.cpu().numpy()
+            hd = p.hist_def.cpu().numpy()
+            for it in range(done_before, k):
+                if not np.isnan(hd[it % chunk]):
+                    state.force_history.append(abs(float(hd[it % chunk])))
+                state.residual_history.append(float(hr[it % chunk]))
+            state.outer_iterations = k
+            done_before = k
+            steps = chunk
+            if d["done"] == DRIVE_RUNNING:
+                continue
+            if d["done"] == DRIVE_CONVERGED:
+                return state
+            if d["done"] == DRIVE_BREAKDOWN:
+                raise FactorizationBreakdownError(-1, "every rung of a point line solve broke down")
+            if d["done"] == DRIVE_NONFINITE:
+                raise PaqifError("non-finite change in point-contact sweep")
+            res = state.residual_history[-1]
+            if d["done"] == DRIVE_DIVERGING:
+                raise NonConvergenceError("contact iteration diverging", residual=res,
+                                          iterations=k)
+            raise NonConvergenceError("contact iteration exhausted its budget", residual=res,
+                                      iterations=max_outer)
+
 
 def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: float = 1 / 3,
               limiter: str = "kappa", tol: float = 1e-6, tol_fb: float = 1e-4,
@@ -148,7 +191,7 @@ def solve_ehl(params: EhlParams, intervals: int, scheme: str = "Lhs1", kappa: fl
     grow = 0
     best = np.inf
     try:
-        if isinstance(drv, _LineDriver) and collect is None and max_outer > 0:
+        if collect is None and max_outer > 0:
             return drv.run(state, tol, tol_fb, max_outer)
         for outer in range(max_outer):
             res, fb = drv.step()

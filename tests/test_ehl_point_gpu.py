@@ -180,3 +180,50 @@ def test_batched_deferred_runs_match_line_by_line(monkeypatch, n, steps):
     assert np.array_equal(s1["newton"], s0["newton"])
     assert np.array_equal(s1["x_rungs"], s0["x_rungs"])
     assert int(np.sum(np.asarray(s1["newton"]) == 0)) >= 4, "no deferred run to batch"
+
+
+@pytest.mark.parametrize("tol,tol_fb,max_outer", [(1e30, 1e30, 12), (0.0, 0.0, 11),
+                                                  (1e30, 1e-300, 10)])
+def test_point_device_driver_matches_host_loop(tol, tol_fb, max_outer):
+    """solve_ehl for a point contact without `collect` runs the loop on the
+    device (paqif_ehl_point_drive_steps: stop / divergence tests after every
+    iteration, force balance on the record's schedule, later iterations of
+    a stopped chunk no-ops); with `collect` the host steps.  Same residual
+    and force histories, state and outcome."""
+    from paper_2008_03276_b200.ehl import solve_ehl
+    from paper_2008_03276_b200.errors import NonConvergenceError
+    p = params_for(100.0)
+    out = []
+    for collect in (None, lambda st, r, d: None):
+        err, st = None, None
+        try:
+            st = solve_ehl(p, 32, tol=tol, tol_fb=tol_fb, max_outer=max_outer, collect=collect)
+        except NonConvergenceError as e:
+            err = (e.iterations, e.residual)
+        out.append((err, st))
+    (e_dev, s_dev), (e_host, s_host) = out
+    assert e_dev == e_host
+    if s_dev is not None:
+        assert s_dev.residual_history == s_host.residual_history
+        assert s_dev.force_history == s_host.force_history
+        assert s_dev.outer_iterations == s_host.outer_iterations
+        assert np.array_equal(s_dev.u, s_host.u) and s_dev.h0 == s_host.h0
+
+
+def test_point_drive_stopped_chunk_is_noop():
+    """A record that is already done turns a whole enqueued chunk into
+    no-ops: the state does not move."""
+    from paper_2008_03276_b200.ehl import PointContact
+    pc = PointContact(params_for(100.0), 32)
+    pc.drive_init(1e30, 1e30, 3, hist_cap=8)
+    pc.drive_steps(6)
+    d = pc.drive_state()
+    assert d["done"] == 3 and d["outer"] == 3
+    s1 = pc.snapshot()
+    pc.drive_steps(4)
+    d2 = pc.drive_state()
+    s2 = pc.snapshot()
+    assert d2["outer"] == 3 and np.array_equal(s1["u"], s2["u"]) and s1["h0"] == s2["h0"]
+    pc.step()  # an explicit step runs again
+    assert not np.array_equal(pc.snapshot()["u"], s2["u"])
+    pc.close()
