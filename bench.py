@@ -315,8 +315,8 @@ def ehl_secondary(rank, world, with_cpu, max_over_ranks, barrier, steps1=200, st
         rate, sample = config3_cpu_pool(cases, threads)
         out["config3"]["cpu_baseline"] = {"value": rate, "unit": "case-iters/s",
                                           "cores": threads, "kind": "port", "sample": sample}
-    if world == 1:
-        out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1]))
+    out.update(point_secondary(with_cpu, steps4=point_steps[0], steps5=point_steps[1],
+                               world=world, max_over_ranks=max_over_ranks, barrier=barrier))
     for v in out.values():
         v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
     if world == 1:
@@ -346,40 +346,77 @@ def tvd_secondary(intervals=256, sweeps=4):
             "residual_last": hist[-1], "arith": "exact (reference rounding)"}
 
 
-def point_secondary(with_cpu, steps4=3, steps5=1):
+def fold_bytes(n):
+    """Algorithmic HBM bytes of one full point deformation (the fold): read
+    the pressure, write the deformation, read the kernel spectrum once
+    ((P/2+1) x P complex, P = next power of two >= 2n)."""
+    P = 32
+    while P < 2 * n:
+        P *= 2
+    N = n + 1
+    return 2 * N * N * 8 + (P // 2 + 1) * P * 16, P
+
+
+def point_secondary(with_cpu, steps4=3, steps5=1, world=1, max_over_ranks=None, barrier=None):
     """EHL point contact, one outer iteration of solve_ehl per step through
     the native sweep driver (csrc/ehl_point.cu): config 4 (513^2, M=100) and
-    config 5 (2049^2, M=1000), device-timed on the handle's stream."""
+    config 5 (2049^2, M=1000), device-timed on the handle's stream; plus the
+    full deformation (fold) alone with its HBM roofline fraction.  With
+    several ranks only config 5 runs: every rank the same contact, each fold
+    split over the ranks (PointContact.shard_folds, csrc/fft_shard.cuh)."""
     import torch
     from paper_2008_03276_b200.ehl import EhlParams, PointContact
     out = {}
+    mor = max_over_ranks or (lambda x: x)
+    bar = barrier or (lambda: None)
+    peaks = load_peaks()
 
-    def run(n, m, steps, warm, exact=True):
+    def run(n, m, steps, warm, exact=True, shard=False, fold_reps=0):
         p = EhlParams.point_from_moes(m, 10.0, domain=(-4.5, 1.5), lo_y=-3.0)
         pc = PointContact(p, n, exact=exact)
+        if shard:
+            pc.shard_folds()
+        stream = torch.cuda.ExternalStream(pc.stream_handle())
         for _ in range(warm):
             pc.step()
         pc.sync()
+        bar()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        stream = torch.cuda.ExternalStream(pc.stream_handle())
         e0.record(stream)
         for _ in range(steps):
             pc.step()
         e1.record(stream)
         e1.synchronize()
-        ms = e0.elapsed_time(e1) / steps
+        ms = mor(e0.elapsed_time(e1) / steps)
+        fold_ms = None
+        if fold_reps:
+            pc.fold_bench(2)
+            pc.sync()
+            bar()
+            e0.record(stream)
+            pc.fold_bench(fold_reps)
+            e1.record(stream)
+            e1.synchronize()
+            fold_ms = mor(e0.elapsed_time(e1) / fold_reps)
         snap = pc.snapshot()
         pc.close()
-        return ms, snap
+        return ms, snap, fold_ms
 
-    if steps4 > 0:
-        ms4, s4 = run(512, 100.0, steps4, 3)
+    def fold_line(n, fold_ms):
+        b, P = fold_bytes(n)
+        gbs = b / (fold_ms * 1e-3) / 1e9
+        return {"ms": fold_ms, "period": P, "algorithmic_bytes": b,
+                "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]}}
+
+    if steps4 > 0 and world == 1:
+        ms4, s4, f4 = run(512, 100.0, steps4, 3, fold_reps=20)
         out["config4"] = {"metric": "EHL point Newton iters/s (513x513, M=100, L=10)",
                           "value": 1e3 / ms4, "unit": "iters/s", "ms_per_iter": ms4,
                           "lines_per_iter": 2 * 511, "newton_x_lines_last": int(s4["newton"].sum()),
-                          "residual_last": s4["res"]}
-        ms4f, s4f = run(512, 100.0, steps4, 3, exact=False)
+                          "residual_last": s4["res"], "fold": fold_line(512, f4)}
+        ms4f, s4f, _ = run(512, 100.0, steps4, 3, exact=False)
         out["config4"]["fma"] = {"ms_per_iter": ms4f, "value": 1e3 / ms4f,
                                  "newton_x_lines_last": int(s4f["newton"].sum())}
         if with_cpu:
@@ -393,13 +430,42 @@ def point_secondary(with_cpu, steps4=3, steps5=1):
                                               "kind": "port",
                                               "sample": "1 oracle point iteration (numpy/scipy)"}
     if steps5 > 0:
-        ms5, s5 = run(2048, 1000.0, steps5, 1)
+        ms5, s5, f5 = run(2048, 1000.0, steps5, 1, shard=world > 1, fold_reps=10)
         out["config5"] = {"metric": "EHL point Newton iters/s (2049x2049, M=1000, L=10)",
                           "value": 1e3 / ms5, "unit": "iters/s", "ms_per_iter": ms5,
-                          "lines_per_iter": 2 * 2047, "residual_last": s5["res"]}
+                          "n_gpus": world, "scaling": "strong",
+                          "folds": "split over the ranks (fft_shard.cuh)" if world > 1
+                                   else "one GPU",
+                          "lines_per_iter": 2 * 2047, "residual_last": s5["res"],
+                          "fold": fold_line(2048, f5)}
+        if with_cpu:
+            out["config5"]["cpu_baseline"] = config5_cpu_baseline()
     for v in out.values():
         v["arith"] = "exact (reference rounding); 'fma' = FMA arithmetic (within 1e-9)"
     return out
+
+
+def config5_cpu_baseline(budget_s=30.0):
+    """Config 5's CPU baseline: the numpy oracle's x-sweep lines from the
+    adapted Hertz start on one host core for ~budget_s, scaled to a whole
+    outer iteration (2 x 2047 line solves plus their folds) by the line
+    count.  One full reference iteration takes ~10 min on one core
+    (SURVEY.md 6.3), too long for a bench run; the sample is named."""
+    import oracle.ehl_point_oracle as P
+    c = P.point_case(1000.0, 10.0)
+    t0 = time.perf_counter()
+    f = P.PointFilm(2048, c)
+    u = P.hertz_start(c, f)
+    f.deformation_full(u)
+    setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    lines = P.x_sweep_lines(u, c.h0, c, f, budget_s)
+    dt = time.perf_counter() - t0
+    per_line = dt / max(lines, 1)
+    iter_s = per_line * 2 * 2047
+    return {"value": 1.0 / iter_s, "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": f"{lines} oracle x-sweep lines of the first iteration in {dt:.1f} s "
+                      f"(+{setup:.1f} s set-up), scaled by 4094 lines per iteration"}
 
 
 def shard_inputs(rank, B):

@@ -248,6 +248,27 @@ int paqif_ehl_point_film_lines(paqif_ehl_point *h, int32_t mode, const int32_t *
 /* Deformation of HOST pressure u into HOST out (FilmModel.deformation_full). */
 int paqif_ehl_point_deformation(paqif_ehl_point *h, const double *u, double *out);
 
+/* Config 5 on several GPUs: every rank runs the same
+ * contact (the line chains in the reference's order, replicated); after
+ * attach_peers every full deformation of the handle is split over the
+ * ranks -- row FFTs, column FFTs x kernel spectrum, inverse row FFTs, each
+ * rank its slab, written straight into the peers' buffers over NVLink with
+ * a system-scope barrier between the phases -- bit-identical to the
+ * one-GPU fold.  ipc_handles: this handle's 3 x 64-byte CUDA IPC handles;
+ * attach_peers: all ranks' handles (world x 3 x 64 bytes, rank order),
+ * world <= 8.  A peer that never reaches a barrier sets err bit 64
+ * (PaqifError) after ~seconds instead of hanging. */
+int paqif_ehl_point_ipc_handles(paqif_ehl_point *h, void *out /*[host] 192 bytes*/);
+int paqif_ehl_point_attach_peers(paqif_ehl_point *h, int32_t rank, int32_t world,
+                                 const void *handles /*[host] world x 192 bytes*/);
+/* test: the sharded decomposition with `world` ranks emulated in order on
+ * one GPU, deformation of u [host] into out [host] */
+int paqif_ehl_point_fold_emulated(paqif_ehl_point *h, int32_t world, const double *u,
+                                  double *out);
+/* bench: `reps` forced folds of the resident pressure (sharded when
+ * attached), enqueued on the handle's stream */
+int paqif_ehl_point_fold_bench(paqif_ehl_point *h, int32_t reps);
+
 /* Deformation kernel tables on the device (ehl/kernels.py:64-100,
  * kernel_line / kernel_point): table [dev] nx+1 doubles, the cell integrals
  * of log|x - x'| for offsets 0..nx; or (nx+1) x (ny+1) row-major, the

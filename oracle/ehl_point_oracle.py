@@ -299,6 +299,35 @@ def hybrid_x_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="k
     return u, tags, rungs
 
 
+def x_sweep_lines(u, h0, c: PointCase, film: PointFilm, budget_s, kappa=1 / 3,
+                  limiter="kappa", variant="Lhs1"):
+    """A bounded sample of hybrid_x_sweep for CPU-baseline timing (bench.py
+    config 5): the sweep's lines in order, Newton lines updating u and the
+    pending list (folds included) as in hybrid_x_sweep, until budget_s
+    seconds have passed.  Returns the number of lines done."""
+    import time
+    n = u.shape[0] - 1
+    h = film.h
+    ns, ws = ("Ls1", "Ls4") if variant == "Lhs1" else ("Ls0", "Ls5")
+    t0 = time.perf_counter()
+    done = 0
+    for j in range(1, n):
+        args, eps_line = line_quantities(u, film, c, j, h0, kappa, limiter)
+        newton = float(np.min(eps_line)) / h > SWITCH
+        sig, _ = robust_solve(args, film, h, kappa, limiter, ns if newton else ws)
+        if newton:
+            sig = np.clip(sig, -c.max_change, c.max_change)
+            new = np.maximum(0.0, u[j, 1:n] + c.omega * sig)
+            delta = np.zeros(n + 1)
+            delta[1:n] = new - u[j, 1:n]
+            u[j, 1:n] = new
+            film.note("row", j, delta, u)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    return done
+
+
 def newton_line_sweep(u, h0, film: PointFilm, c: PointCase, kappa=1 / 3, limiter="kappa",
                       scheme="Ls1", omega=None, hybrid=None):
     """sweeps.newton_line_sweep (sweeps.py:344-379): immediate updates, the

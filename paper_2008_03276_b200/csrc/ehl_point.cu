@@ -20,6 +20,7 @@
 #include "aqif2.cuh"
 #include "aqif1.cuh"
 #include "fft_deform.cuh"
+#include "fft_shard.cuh"
 #include "capi_util.cuh"
 
 extern "C" {
@@ -815,7 +816,7 @@ __global__ void pt_drive_kernel(PointDev d, paqif_ehl_point_cfg c, paqif_ehl_lin
     d.meta[kMStop] = 1;
     return;
   }
-  if (err & 10) {
+  if (err & (10 | 64)) {  // non-finite change, or a sharded fold lost a peer
     r.done = 5;
     d.meta[kMStop] = 1;
     return;
@@ -866,6 +867,11 @@ struct paqif_ehl_point {
   bool xinfo_valid = false;
   bool runs = true;  // PAQIF_PT_RUNS=0 solves every x-line on its own (A/B checks)
   std::vector<int32_t> pred;  // run-prediction tags for a device-driven chunk
+  // sharded folds across ranks (fft_shard.cuh), after attach_peers
+  unsigned* bar = nullptr;    // this rank's barrier words
+  bool sharded = false;
+  FoldPeers peers{};
+  std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -880,6 +886,11 @@ T* dalloc(paqif_ehl_point* h, size_t count) {
 }
 
 void fold(paqif_ehl_point* h) {
+  if (h->sharded) {  // split over the ranks (fft_shard.cuh)
+    fold_sharded(h->plan, h->d.u, h->peers, &h->d.meta[kMGate], &h->d.meta[kMCount],
+                 &h->d.meta[kMErr], h->st);
+    return;
+  }
   // one cooperative launch; a no-op (gate == 0) costs one empty kernel
   fft_fold(h->plan, h->d.u, h->d.dbase, &h->d.meta[kMGate], &h->d.meta[kMCount], h->st);
 }
@@ -945,6 +956,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
   d.done = dalloc<int32_t>(h, N);
   d.run_scratch = dalloc<double>(h, d.sys_in_smem ? 32 : (size_t)kRunCtas * pt_sys_doubles(n_sys));
   d.fpart = dalloc<double>(h, (size_t)kMaxPending * kFilmSegMax * 4 * N);
+  h->bar = dalloc<unsigned>(h, 64);
   if (const char* e = getenv("PAQIF_PT_RUNS")) h->runs = e[0] != '0';
   d.prof = nullptr;
   if (const char* e = getenv("PAQIF_PT_PROF"))
@@ -955,7 +967,7 @@ extern "C" paqif_ehl_point* paqif_ehl_point_create(const paqif_ehl_point_cfg* cf
       set_cuda_error("ehl_point: alloc", cudaErrorMemoryAllocation);
       return nullptr;
     }
-  if (h->allocs.size() != (d.prof ? 21u : 20u) ||
+  if (h->allocs.size() != (d.prof ? 22u : 21u) ||
       cudaMallocHost((void**)&h->xinfo_prev, (size_t)N * sizeof(int32_t)) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->xinfo_ev, cudaEventDisableTiming) != cudaSuccess) {
     paqif_ehl_point_destroy(h);
@@ -993,6 +1005,7 @@ extern "C" void paqif_ehl_point_destroy(paqif_ehl_point* h) {
             "; levels %llu, with a tiny numerator %llu\n",
             ap[4], ap[0] / na, ap[1] / na, ap[2] / na, ap[3] / na, ap[5], ap[6]);
   }
+  for (void* a : h->ipc_opened) cudaIpcCloseMemHandle(a);
   for (void* a : h->allocs)
     if (a) cudaFree(a);
   if (h->xinfo_prev) cudaFreeHost(h->xinfo_prev);
@@ -1344,3 +1357,81 @@ extern "C" int paqif_ehl_point_film_lines(paqif_ehl_point* h, int32_t mode, cons
   return e == cudaSuccess ? check_launch("ehl_point_film_lines") : set_cuda_error("film_lines", e);
 }
 
+
+// ------------------------------------------------------- sharded folds
+// IPC handles of this handle's buffers the peers write into: the
+// half-spectrum buffer W, the deformation base D and the barrier words
+// (3 x 64 bytes).
+extern "C" int paqif_ehl_point_ipc_handles(paqif_ehl_point* h, void* out) {
+  if (!h || !out) return set_arg_error("ehl_point_ipc_handles");
+  cudaIpcMemHandle_t* o = reinterpret_cast<cudaIpcMemHandle_t*>(out);
+  cudaError_t e;
+  if ((e = cudaIpcGetMemHandle(&o[0], h->plan.W)) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle(&o[1], h->d.dbase)) != cudaSuccess ||
+      (e = cudaIpcGetMemHandle(&o[2], h->bar)) != cudaSuccess)
+    return set_cuda_error("ehl_point_ipc_handles", e);
+  return PAQIF_OK;
+}
+
+// Open every peer's handles (world x 3 x 64 bytes, in rank order) and split
+// every later fold of this handle over the ranks.  All ranks attach before
+// any of them folds again (the caller's exchange of handles is that sync).
+extern "C" int paqif_ehl_point_attach_peers(paqif_ehl_point* h, int32_t rank, int32_t world,
+                                            const void* handles) {
+  if (!h || !handles || world < 1 || world > kFoldMaxRanks || rank < 0 || rank >= world)
+    return set_arg_error("ehl_point_attach_peers: rank / world (1..8)");
+  if (h->sharded) return set_arg_error("ehl_point_attach_peers: already attached");
+  const cudaIpcMemHandle_t* in = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  FoldPeers q{};
+  q.rank = rank;
+  q.world = world;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      q.W[r] = h->plan.W;
+      q.D[r] = h->d.dbase;
+      q.bar[r] = h->bar;
+      continue;
+    }
+    void* ptr[3];
+    for (int b = 0; b < 3; ++b) {
+      cudaError_t e = cudaIpcOpenMemHandle(&ptr[b], in[3 * r + b], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return set_cuda_error("ehl_point_attach_peers: open", e);
+      h->ipc_opened.push_back(ptr[b]);
+    }
+    q.W[r] = reinterpret_cast<double2*>(ptr[0]);
+    q.D[r] = reinterpret_cast<double*>(ptr[1]);
+    q.bar[r] = reinterpret_cast<unsigned*>(ptr[2]);
+  }
+  h->peers = q;
+  h->sharded = world > 1;
+  return PAQIF_OK;
+}
+
+// Dev / test: the sharded decomposition with `world` ranks emulated in
+// order on this GPU, deformation of u (host, N x N) into out (host) --
+// bit-identical to paqif_ehl_point_deformation for every world.
+extern "C" int paqif_ehl_point_fold_emulated(paqif_ehl_point* h, int32_t world, const double* u,
+                                             double* out) {
+  if (!h || !u || world < 1 || world > 64) return set_arg_error("ehl_point_fold_emulated");
+  const size_t NN = (size_t)h->d.N * h->d.N;
+  cudaMemcpyAsync(h->d.film_out, u, NN * 8, cudaMemcpyHostToDevice, h->st);
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
+  pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
+  fold_sharded_emulated(h->plan, h->d.film_out, h->d.dbase, world, &h->d.meta[kMGate],
+                        &h->d.meta[kMCount], h->st);
+  if (out) cudaMemcpyAsync(out, h->d.dbase, NN * 8, cudaMemcpyDeviceToHost, h->st);
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  return e == cudaSuccess ? check_launch("ehl_point_fold_emulated") : set_cuda_error("fold_emulated", e);
+}
+
+// Bench: `reps` forced folds of the resident pressure (sharded when
+// attached), enqueued on the handle's stream.
+extern "C" int paqif_ehl_point_fold_bench(paqif_ehl_point* h, int32_t reps) {
+  if (!h || reps < 0) return set_arg_error("ehl_point_fold_bench");
+  cudaMemsetAsync(&h->d.meta[kMStop], 0, sizeof(int), h->st);
+  for (int r = 0; r < reps; ++r) {
+    pt_set_gate_kernel<<<1, 32, 0, h->st>>>(h->d.meta, 0);
+    fold(h);
+  }
+  return check_launch("paqif_ehl_point_fold_bench");
+}

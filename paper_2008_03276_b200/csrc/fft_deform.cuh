@@ -140,6 +140,90 @@ __device__ __forceinline__ void fft_dit_smem(double2* x, int L, int logL, const 
   }
 }
 
+// The three phases, per row / column, shared by the one-kernel fold and the
+// sharded fold (fft_shard.cuh): the same arithmetic whichever block or GPU
+// computes a row or column, so the results are bit-identical.
+// Phase R, row r: half spectrum of the real row (plan_mode: of the mirrored
+// table) -> out[0..H].  buf: P double2 of shared memory, twd: staged twiddles.
+__device__ __forceinline__ void fold_row_r(const FftPlan& p, const double* __restrict__ src, int r,
+                                           int plan_mode, double2* buf, const double2* twd,
+                                           double2* out) {
+  const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1, n = p.n, N = n + 1;
+  const int rows = plan_mode ? (2 * n + 1 < P ? 2 * n + 1 : P) : N;
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    const int c0 = 2 * c, c1 = 2 * c + 1;
+    double v0 = 0.0, v1 = 0.0;
+    if (!plan_mode) {
+      const double* row = src + (size_t)r * N;
+      if (c0 < N) v0 = row[c0];
+      if (c1 < N) v1 = row[c1];
+    } else {
+      const double* row = src + (size_t)abs(r - n) * N;
+      if (c0 < rows) v0 = row[abs(c0 - n)];
+      if (c1 < rows) v1 = row[abs(c1 - n)];
+    }
+    buf[c] = make_double2(v0, v1);
+  }
+  __syncthreads();
+  fft_dif_smem(buf, H, logH, twd, logP, 0);
+  for (int k = threadIdx.x; k <= H; k += blockDim.x) {
+    const double2 zk = buf[bitrev(k & (H - 1), logH)];
+    const double2 zm = buf[bitrev((H - k) & (H - 1), logH)];
+    const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+    const double2 o = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    const double2 w = k < H ? twd[k] : make_double2(-1.0, 0.0);
+    out[k] = cadd(e, cmul(w, o));
+  }
+  __syncthreads();
+}
+
+// Phase C, column k: load W[.][k] (rows >= `rows` zero), forward FFT; plan
+// mode stores the spectrum in KT, else multiplies by it, inverse FFT and
+// leaves the N output rows n..2n (wrapped) in buf[wrap(m)] for the caller.
+__device__ __forceinline__ void fold_col_c(const FftPlan& p, const double2* __restrict__ Wsrc,
+                                           int k, int rows, int plan_mode, double2* buf,
+                                           const double2* twd) {
+  const int P = p.P, logP = p.logP, ld = (P >> 1) + 1;
+  for (int r = threadIdx.x; r < P; r += blockDim.x)
+    buf[r] = r < rows ? Wsrc[(size_t)r * ld + k] : make_double2(0.0, 0.0);
+  __syncthreads();
+  fft_dif_smem(buf, P, logP, twd, logP, 0);
+  double2* kt = p.KT + (size_t)k * P;
+  if (plan_mode) {
+    for (int j = threadIdx.x; j < P; j += blockDim.x) kt[j] = buf[j];
+    __syncthreads();
+    return;
+  }
+  for (int j = threadIdx.x; j < P; j += blockDim.x) buf[j] = cmul(buf[j], kt[j]);
+  __syncthreads();
+  fft_dit_smem(buf, P, logP, twd, logP, 1);
+}
+__device__ __forceinline__ int fold_wrap(int m, int n, int P) {
+  return m + n < P ? m + n : m + n - P;  // row 2n wraps to 0 when P = 2n
+}
+
+// Phase I, output row m: merge the half spectrum in[0..H] and inverse FFT;
+// the N outputs are ((c & 1) ? buf[c >> 1].y : .x) * scale, c = wrap(i).
+__device__ __forceinline__ void fold_row_i(const FftPlan& p, const double2* __restrict__ in,
+                                           double2* buf, const double2* twd) {
+  const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) {
+    const double2 yk = in[k], ym = in[H - k];
+    const double2 e = make_double2(0.5 * (yk.x + ym.x), 0.5 * (yk.y - ym.y));
+    const double2 o = cmul(make_double2(0.5 * (yk.x - ym.x), 0.5 * (yk.y + ym.y)),
+                           tw_at(twd, k, 1));
+    buf[bitrev(k, logH)] = make_double2(e.x - o.y, e.y + o.x);
+  }
+  __syncthreads();
+  fft_dit_smem(buf, H, logH, twd, logP, 1);
+}
+__device__ __forceinline__ double fold_out(const double2* buf, int i, int n, int P,
+                                           double scale) {
+  const int c = fold_wrap(i, n, P);
+  const double2 v = buf[c >> 1];
+  return ((c & 1) ? v.y : v.x) * scale;
+}
+
 // plan_mode 0: D = deformation(src = u, N x N), gated; clears the gate and the
 // pending count.  plan_mode 1: KT = spectrum of the mirrored table (src).
 // Dynamic smem: P + P/2 double2.
@@ -150,7 +234,7 @@ __global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* 
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double2 fsm[];
-  const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1, n = p.n, N = n + 1;
+  const int P = p.P, H = P >> 1, n = p.n, N = n + 1;
   const int ld = H + 1;
   double2* buf = fsm;
   double2* twd = fsm + P;
@@ -158,55 +242,16 @@ __global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* 
   const int rows = plan_mode ? (2 * n + 1 < P ? 2 * n + 1 : P) : N;
 
   // ---- R: half spectra of the real rows
-  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-    for (int c = threadIdx.x; c < H; c += blockDim.x) {
-      const int c0 = 2 * c, c1 = 2 * c + 1;
-      double v0 = 0.0, v1 = 0.0;
-      if (!plan_mode) {
-        const double* row = src + (size_t)r * N;
-        if (c0 < N) v0 = row[c0];
-        if (c1 < N) v1 = row[c1];
-      } else {
-        const double* row = src + (size_t)abs(r - n) * N;
-        if (c0 < rows) v0 = row[abs(c0 - n)];
-        if (c1 < rows) v1 = row[abs(c1 - n)];
-      }
-      buf[c] = make_double2(v0, v1);
-    }
-    __syncthreads();
-    fft_dif_smem(buf, H, logH, twd, logP, 0);
-    double2* out = p.W + (size_t)r * ld;
-    for (int k = threadIdx.x; k <= H; k += blockDim.x) {
-      const double2 zk = buf[bitrev(k & (H - 1), logH)];
-      const double2 zm = buf[bitrev((H - k) & (H - 1), logH)];
-      const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-      const double2 o = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-      const double2 w = k < H ? twd[k] : make_double2(-1.0, 0.0);
-      out[k] = cadd(e, cmul(w, o));
-    }
-    __syncthreads();
-  }
+  for (int r = blockIdx.x; r < rows; r += gridDim.x)
+    fold_row_r(p, src, r, plan_mode, buf, twd, p.W + (size_t)r * ld);
   grid.sync();
 
   // ---- C: column transforms, kernel product, inverse, output rows
   for (int k = blockIdx.x; k <= H; k += gridDim.x) {
-    for (int r = threadIdx.x; r < P; r += blockDim.x)
-      buf[r] = r < rows ? p.W[(size_t)r * ld + k] : make_double2(0.0, 0.0);
-    __syncthreads();
-    fft_dif_smem(buf, P, logP, twd, logP, 0);
-    double2* kt = p.KT + (size_t)k * P;
-    if (plan_mode) {
-      for (int j = threadIdx.x; j < P; j += blockDim.x) kt[j] = buf[j];
-      __syncthreads();
-      continue;
-    }
-    for (int j = threadIdx.x; j < P; j += blockDim.x) buf[j] = cmul(buf[j], kt[j]);
-    __syncthreads();
-    fft_dit_smem(buf, P, logP, twd, logP, 1);
-    for (int m = threadIdx.x; m < N; m += blockDim.x) {
-      const int r = m + n < P ? m + n : m + n - P;  // row 2n wraps to 0 when P = 2n
-      p.W[(size_t)m * ld + k] = buf[r];
-    }
+    fold_col_c(p, p.W, k, rows, plan_mode, buf, twd);
+    if (plan_mode) continue;
+    for (int m = threadIdx.x; m < N; m += blockDim.x)
+      p.W[(size_t)m * ld + k] = buf[fold_wrap(m, n, P)];
     __syncthreads();
   }
   if (plan_mode) return;
@@ -215,22 +260,9 @@ __global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* 
   // ---- I: real output rows from their half spectra
   const double scale = 1.0 / ((double)P * (double)H);
   for (int m = blockIdx.x; m < N; m += gridDim.x) {
-    const double2* in = p.W + (size_t)m * ld;
-    for (int k = threadIdx.x; k < H; k += blockDim.x) {
-      const double2 yk = in[k], ym = in[H - k];
-      const double2 e = make_double2(0.5 * (yk.x + ym.x), 0.5 * (yk.y - ym.y));
-      const double2 o = cmul(make_double2(0.5 * (yk.x - ym.x), 0.5 * (yk.y + ym.y)),
-                             tw_at(twd, k, 1));
-      buf[bitrev(k, logH)] = make_double2(e.x - o.y, e.y + o.x);
-    }
-    __syncthreads();
-    fft_dit_smem(buf, H, logH, twd, logP, 1);
+    fold_row_i(p, p.W + (size_t)m * ld, buf, twd);
     double* out = D + (size_t)m * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      const int c = i + n < P ? i + n : i + n - P;
-      const double2 v = buf[c >> 1];
-      out[i] = ((c & 1) ? v.y : v.x) * scale;
-    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) out[i] = fold_out(buf, i, n, P, scale);
     __syncthreads();
   }
   grid.sync();

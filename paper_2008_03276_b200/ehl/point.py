@@ -71,6 +71,14 @@ def _bind(L):
     L.paqif_ehl_point_film_lines.argtypes = [vp, ctypes.c_int32, vp, ctypes.c_int32,
                                              ctypes.c_double, vp]
     L.paqif_ehl_point_film_lines.restype = ctypes.c_int
+    L.paqif_ehl_point_ipc_handles.argtypes = [vp, vp]
+    L.paqif_ehl_point_ipc_handles.restype = ctypes.c_int
+    L.paqif_ehl_point_attach_peers.argtypes = [vp, i32, i32, vp]
+    L.paqif_ehl_point_attach_peers.restype = ctypes.c_int
+    L.paqif_ehl_point_fold_emulated.argtypes = [vp, i32, vp, vp]
+    L.paqif_ehl_point_fold_emulated.restype = ctypes.c_int
+    L.paqif_ehl_point_fold_bench.argtypes = [vp, i32]
+    L.paqif_ehl_point_fold_bench.restype = ctypes.c_int
     L._ehl_point_bound = True
     return L
 
@@ -143,6 +151,17 @@ class PointDevice:
         _native.check(rc, "paqif_ehl_point_deformation")
         return out
 
+    def fold_emulated(self, world: int, u) -> np.ndarray:
+        """The sharded fold's decomposition over `world` ranks emulated in
+        order on this GPU (test of the slab arithmetic; fft_shard.cuh)."""
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        if uu.shape != (self.n + 1, self.n + 1):
+            raise ContractViolationError("u must be (n+1, n+1)")
+        out = np.empty_like(uu)
+        rc = self.h.L.paqif_ehl_point_fold_emulated(self.h.ptr, int(world), _ptr(uu), _ptr(out))
+        _native.check(rc, "paqif_ehl_point_fold_emulated")
+        return out
+
     def note_update(self, axis: int, index: int, delta) -> None:
         """Append a pending line update (device list; see FilmModel)."""
         dd = np.ascontiguousarray(delta, dtype=np.float64)
@@ -213,6 +232,38 @@ class PointContact:
         rc = self.L.paqif_ehl_point_step(self._h.ptr, self.outer, self.flags)
         _native.check(rc, "paqif_ehl_point_step")
         self.outer += 1
+
+    def shard_folds(self, group=None) -> int:
+        """Config 5 on several GPUs: split every later full deformation of
+        this contact over the ranks of `group` (torch.distributed, one rank
+        per GPU, every rank running the same contact): the handles' CUDA IPC
+        handles are exchanged with all_gather_object and each rank's fold
+        phases write straight into the peers' buffers (fft_shard.cuh).
+        Returns the world size (1: nothing to do)."""
+        import torch.distributed as dist
+        if not dist.is_available() or not dist.is_initialized():
+            return 1
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world == 1:
+            return 1
+        if world > 8:
+            raise ContractViolationError("sharded folds: at most 8 ranks")
+        self.sync()
+        mine = ctypes.create_string_buffer(192)
+        _native.check(self.L.paqif_ehl_point_ipc_handles(self._h.ptr, mine),
+                      "paqif_ehl_point_ipc_handles")
+        got = [None] * world
+        dist.all_gather_object(got, bytes(mine.raw), group=group)
+        blob = ctypes.create_string_buffer(b"".join(got), 192 * world)
+        _native.check(self.L.paqif_ehl_point_attach_peers(self._h.ptr, rank, world, blob),
+                      "paqif_ehl_point_attach_peers")
+        dist.barrier(group=group)  # every rank attached before anyone folds
+        return world
+
+    def fold_bench(self, reps: int) -> None:
+        """Enqueue `reps` forced full deformations (sharded when attached)."""
+        _native.check(self.L.paqif_ehl_point_fold_bench(self._h.ptr, int(reps)),
+                      "paqif_ehl_point_fold_bench")
 
     def drive_init(self, tol: float, tol_fb: float, max_outer: int, hist_cap: int = 16):
         """Device solve_ehl record (the line contact's layout, DRIVE_DTYPE):
@@ -305,6 +356,8 @@ class PointContact:
             raise FactorizationBreakdownError(-1, "every rung of a point line solve broke down")
         if err & 10:
             raise PaqifError("non-finite change in point-contact sweep")
+        if err & 64:
+            raise PaqifError("sharded fold: a peer rank did not reach the barrier")
 
     def close(self) -> None:
         self._h.close()

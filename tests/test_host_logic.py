@@ -309,3 +309,52 @@ class TestTvdHost:
         r1 = prob.residual_field(exact)
         r2 = twin.residual_field(np.ascontiguousarray(exact.T))
         assert np.allclose(r1, r2.T, atol=1e-12)
+
+
+def _shard_attach_worker(rank, world, port, q):
+    """One rank of PointContact.shard_folds over gloo with the native calls
+    mocked: every rank must receive all ranks' IPC handles in rank order."""
+    import ctypes
+    import torch.distributed as dist
+    from paper_2008_03276_b200.ehl.point import PointContact
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    class FakeL:
+        attached = None
+
+        def paqif_ehl_point_ipc_handles(self, ptr, buf):
+            ctypes.memmove(buf, bytes([rank + 1]) * 192, 192)
+            return 0
+
+        def paqif_ehl_point_attach_peers(self, ptr, r, w, blob):
+            FakeL.attached = (r, w, bytes(blob.raw))
+            return 0
+
+    class FakeH:
+        ptr = 1
+
+    pc = object.__new__(PointContact)
+    pc.L, pc._h = FakeL(), FakeH()
+    pc.sync = lambda: None
+    w = pc.shard_folds()
+    q.put((rank, w, FakeL.attached))
+    dist.destroy_process_group()
+
+
+def test_shard_folds_handle_exchange_gloo():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_attach_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+    expect = b"".join(bytes([r + 1]) * 192 for r in range(3))
+    for rank, w, (r, wa, blob) in got:
+        assert w == 3 and wa == 3 and r == rank
+        assert blob == expect
