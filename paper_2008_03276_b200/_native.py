@@ -13,7 +13,7 @@ import os
 from .errors import PaqifError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libpaqif_b200.so")
+LIB_PATH = os.environ.get("PAQIF_LIB") or os.path.join(HERE, "_build", "libpaqif_b200.so")
 
 FLAG_EXACT = 1
 FLAG_LINE_SPLIT = 2   # EHL line steps: force the split three-kernel path

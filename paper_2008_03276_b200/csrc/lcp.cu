@@ -303,6 +303,24 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         active = false;
       }
       PAQIF_TSTAMP(t2);
+      if (!SOLVE_ONLY && active) {
+        // the band and f into L2 while the Z chain runs, for the
+        // complementarity check that follows it (one bulk prefetch per lane)
+        const size_t bytes = nb * 8;
+        const size_t chunk = ((bytes + G - 1) / G + 15) & ~(size_t)15;
+        const size_t lo = (size_t)gl * chunk;
+        if (lo < bytes) {
+          const size_t len = bytes - lo < chunk ? bytes - lo : chunk;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                           reinterpret_cast<const char*>(bd) + lo),
+                       "r"((unsigned)len)
+                       : "memory");
+        }
+        if (gl == G - 1)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(fb),
+                       "r"((unsigned)(n * 8))
+                       : "memory");
+      }
       if (const int zst = zsolve_group<BETA, EXACT, false>(zs, n, x, my_sm.post.scratch, gl, active)) {
         st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
         brk_level = zst;

@@ -14,6 +14,8 @@
 
 namespace paqif {
 
+constexpr int kZPrefetch = 4;  // record chunks prefetched into L2 ahead of the ring
+
 template <int BETA>
 struct ZChunk {
   static constexpr int ZC = BETA * ((8 + BETA - 1) / BETA);  // levels per chunk, multiple of BETA
@@ -53,17 +55,20 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
                           xr[(ph - 1 - t + 2 * BETA) % BETA]);
     }
   } else {
-    // FMA arithmetic: the terms of the older unknowns first, the two that
-    // the previous level just produced (x[p-1], x[q+1]) last, so only two
-    // FMAs wait on the previous level
+    // FMA arithmetic: the terms of the older unknowns first, in two
+    // independent partial sums (left / right window), the two that the
+    // previous level just produced (x[p-1], x[q+1]) last, so only two FMAs
+    // wait on the previous level and the older terms' chain is half as long
+    double accr = 0.0;
 #pragma unroll
     for (int t = 0; t < BETA; ++t) {
       if (t != BETA - 1 && (!CHECK || p - BETA + t >= 0))
         acc = A::axpy_neg(acc, rec[PL::zi(0, BETA - t, 0) + sd], xl[(ph + t) % BETA]);
       if (t != 0 && (!CHECK || q + 1 + t < n))
-        acc = A::axpy_neg(acc, rec[PL::zi(1, 1 + t, 0) + sd],
-                          xr[(ph - 1 - t + 2 * BETA) % BETA]);
+        accr = A::axpy_neg(accr, rec[PL::zi(1, 1 + t, 0) + sd],
+                           xr[(ph - 1 - t + 2 * BETA) % BETA]);
     }
+    acc = acc + accr;
     if (!CHECK || q + 1 < n)
       acc = A::axpy_neg(acc, rec[PL::zi(1, 1, 0) + sd], xr[(ph - 1 + 2 * BETA) % BETA]);
     if (!CHECK || p - 1 >= 0)
@@ -72,7 +77,8 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
   const double oth = __shfl_xor_sync(pair, acc, 1);
   const double rt = sd == 0 ? acc : oth;
   const double rb = sd == 0 ? oth : acc;
-  if (bad) return false;
+  // no branch on the test: the quotients are computed either way (garbage
+  // after a breakdown, which the caller discards) and the flag returned
   if (EXACT) {
     const bool ds = div_safe(det);
     xp = div_rn(A::det2(a22, rt, a12, rb), det, y, ds);
@@ -81,7 +87,7 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
     xp = (a22 * rt - a12 * rb) * y;
     xq = (a11 * rb - a21 * rt) * y;
   }
-  return true;
+  return !bad;
 }
 
 // All 32 lanes call.  Returns 0 or the 1-based breakdown level.
@@ -113,6 +119,13 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
       const double* src = zs + (size_t)k_lo * RS;
       double* dst = ring + buf * ZC * RS;
       for (int q = gl; q < pieces; q += G) cp_async16(dst + 2 * q, src + 2 * q);
+      // the records a few chunks further down the stack into L2 (written
+      // by the factorization long ago: typically evicted to HBM)
+      const int k_pf = k_lo - (kZPrefetch - 1) * ZC;
+      if (gl == 0 && k_pf >= 1)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(zs + (size_t)k_pf * RS),
+                     "r"((unsigned)(ZC * RS * 8))
+                     : "memory");
     }
     cp_async_commit();
   };
@@ -139,10 +152,7 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
         const bool ok = (FULL && p < BETA)
                             ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
                             : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
-        if (!ok) {
-          status = p + 1;
-          break;
-        }
+        status = (!ok & (status == 0)) ? p + 1 : status;  // first failing level, no branch
         x[sd == 0 ? p : n - 1 - p] = sd == 0 ? xp : xq;
         xl[ph % BETA] = xp;
         xr[ph % BETA] = xq;
