@@ -43,20 +43,64 @@ struct FftPlan {
   double2* tw;  // P/2 twiddles exp(-2 pi i t / P)
 };
 
+// Complex arithmetic with the rounding spelled out (explicit FMA / RN
+// intrinsics): the compiler's contraction choices would otherwise differ
+// between the kernels that inline the same row / column functions (the
+// one-kernel fold and the sharded phases), and bit-identical results across
+// them are part of the contract (fft_shard.cuh).
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
+                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
-  return make_double2(a.x + b.x, a.y + b.y);
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
 }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) {
-  return make_double2(a.x - b.x, a.y - b.y);
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
 }
-__device__ __forceinline__ double2 tw_at(const double2* twd, int idx, int inverse) {
-  const double2 w = twd[idx];
-  return inverse ? make_double2(w.x, -w.y) : w;
-}
+__device__ __forceinline__ double half_(double v) { return __dmul_rn(0.5, v); }
 __device__ __forceinline__ int bitrev(int k, int bits) { return (int)(__brev(k) >> (32 - bits)); }
+
+// Shared-memory position of element i of a transform buffer: the low three
+// index bits (the 16-byte slot within a 128-byte bank row) XOR-folded with
+// every higher 3-bit group.  Bijective; 32 consecutive elements still fill 8
+// distinct slots four times, and so do the strided and bit-reversed access
+// patterns of the short-span stages and of the half-spectrum split (which
+// would otherwise hit one slot: up to 32-way bank conflicts,
+// profiles/fold_ncu_r02.txt).
+__device__ __forceinline__ int sw(int i) {
+  int f = i >> 3;
+  f ^= f >> 3;
+  f ^= f >> 6;
+  f ^= f >> 12;
+  return i ^ (f & 7);
+}
+
+// Twiddles by level: stage tables W_{2^L}^t (t < 2^(L-1)) stored one after
+// the other in shared memory, level L at offset 2^(L-1), for L < logP; the
+// top level (W_P^t) is read from the global table (consecutive t: coalesced,
+// L1-resident).  A butterfly stage reads consecutive t of ONE level, so the
+// shared reads are conflict-free -- the strided reads of a single W_P table
+// (every 2^s-th entry) were 59 % of the fold's excess shared wavefronts
+// (profiles/fold_ncu_r02.txt).  Same values, so the output is unchanged.
+struct Twiddles {
+  const double2* lv;  // shared: levels 1 .. logP-1
+  const double2* top; // global: W_P^t, t < P/2
+  int logP;
+  __device__ __forceinline__ double2 at(int L, int t, int inverse) const {
+    const double2 w = L == logP ? top[t] : lv[(1 << (L - 1)) + t];
+    return inverse ? make_double2(w.x, -w.y) : w;
+  }
+};
+// build the shared levels (P/2 entries, index 0 unused); all threads call
+__device__ __forceinline__ void twiddle_levels(double2* lv, const double2* top, int logP) {
+  const int half = 1 << (logP - 1);
+  for (int idx = 1 + threadIdx.x; idx < half; idx += blockDim.x) {
+    const int L = 32 - __clz(idx);  // 2^(L-1) <= idx < 2^L
+    const int t = idx - (1 << (L - 1));
+    lv[idx] = top[t << (logP - L)];
+  }
+}
 
 __global__ void fft_twiddles(double2* tw, int P) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -68,73 +112,71 @@ __global__ void fft_twiddles(double2* tw, int P) {
 }
 
 // Decimation in frequency, natural order in -> bit-reversed order out, length
-// L = 2^logL <= Ptw = 2^logPtw (twiddle e^{-2 pi i k / (2m)} = twd[k Ptw/(2m)]).
-// Caller synchronises before; ends synchronised.
-__device__ __forceinline__ void fft_dif_smem(double2* x, int L, int logL, const double2* twd,
-                                             int logPtw, int inverse) {
+// L = 2^logL <= P (stage of span m uses the twiddles of levels log2 m and
+// log2 m + 1).  Caller synchronises before; ends synchronised.
+__device__ __forceinline__ void fft_dif_smem(double2* x, int L, int logL, const Twiddles& tw,
+                                             int inverse) {
   int lm = logL - 1;  // m = 2^lm: current butterfly span
   for (; lm >= 1; lm -= 2) {
     const int m = 1 << lm, h = m >> 1;
-    const int sa = logPtw - lm - 1, sb = logPtw - lm;  // twiddle strides (log2)
     for (int j = threadIdx.x; j < L / 4; j += blockDim.x) {
       const int q = j & (h - 1);
       const int base = (j >> (lm - 1)) << (lm + 1);
-      const double2 x0 = x[base + q], x1 = x[base + q + h];
-      const double2 x2 = x[base + q + m], x3 = x[base + q + m + h];
+      const double2 x0 = x[sw(base + q)], x1 = x[sw(base + q + h)];
+      const double2 x2 = x[sw(base + q + m)], x3 = x[sw(base + q + m + h)];
       const double2 a0 = cadd(x0, x2), a1 = cadd(x1, x3);
-      const double2 a2 = cmul(csub(x0, x2), tw_at(twd, q << sa, inverse));
-      const double2 a3 = cmul(csub(x1, x3), tw_at(twd, (q + h) << sa, inverse));
-      const double2 wb = tw_at(twd, q << sb, inverse);
-      x[base + q] = cadd(a0, a1);
-      x[base + q + h] = cmul(csub(a0, a1), wb);
-      x[base + q + m] = cadd(a2, a3);
-      x[base + q + m + h] = cmul(csub(a2, a3), wb);
+      const double2 a2 = cmul(csub(x0, x2), tw.at(lm + 1, q, inverse));
+      const double2 a3 = cmul(csub(x1, x3), tw.at(lm + 1, q + h, inverse));
+      const double2 wb = tw.at(lm, q, inverse);
+      x[sw(base + q)] = cadd(a0, a1);
+      x[sw(base + q + h)] = cmul(csub(a0, a1), wb);
+      x[sw(base + q + m)] = cadd(a2, a3);
+      x[sw(base + q + m + h)] = cmul(csub(a2, a3), wb);
     }
     __syncthreads();
   }
   if (lm == 0) {  // odd log2 L: last span-1 stage, unit twiddles
     for (int j = threadIdx.x; j < L / 2; j += blockDim.x) {
-      const double2 a = x[2 * j], b = x[2 * j + 1];
-      x[2 * j] = cadd(a, b);
-      x[2 * j + 1] = csub(a, b);
+      const double2 a = x[sw(2 * j)], b = x[sw(2 * j + 1)];
+      x[sw(2 * j)] = cadd(a, b);
+      x[sw(2 * j + 1)] = csub(a, b);
     }
     __syncthreads();
   }
 }
 
 // Decimation in time, bit-reversed order in -> natural order out.
-__device__ __forceinline__ void fft_dit_smem(double2* x, int L, int logL, const double2* twd,
-                                             int logPtw, int inverse) {
+__device__ __forceinline__ void fft_dit_smem(double2* x, int L, int logL, const Twiddles& tw,
+                                             int inverse) {
   int s = 0;
   for (; s + 1 < logL; s += 2) {
     const int m = 1 << s;  // stage s pairs (q, q+m); stage s+1 pairs (q, q+2m)
-    const int s0 = logPtw - s - 1, s1 = logPtw - s - 2;
     for (int j = threadIdx.x; j < L / 4; j += blockDim.x) {
       const int q = j & (m - 1);
       const int base = (j >> s) << (s + 2);
-      const double2 w0 = tw_at(twd, q << s0, inverse);
-      const double2 x0 = x[base + q], x1 = x[base + q + m];
-      const double2 x2 = x[base + q + 2 * m], x3 = x[base + q + 3 * m];
+      const double2 w0 = tw.at(s + 1, q, inverse);
+      const double2 x0 = x[sw(base + q)], x1 = x[sw(base + q + m)];
+      const double2 x2 = x[sw(base + q + 2 * m)], x3 = x[sw(base + q + 3 * m)];
       const double2 t1 = cmul(x1, w0), t3 = cmul(x3, w0);
       const double2 a0 = cadd(x0, t1), a1 = csub(x0, t1);
-      const double2 u2 = cmul(cadd(x2, t3), tw_at(twd, q << s1, inverse));
-      const double2 u3 = cmul(csub(x2, t3), tw_at(twd, (q + m) << s1, inverse));
-      x[base + q] = cadd(a0, u2);
-      x[base + q + 2 * m] = csub(a0, u2);
-      x[base + q + m] = cadd(a1, u3);
-      x[base + q + 3 * m] = csub(a1, u3);
+      const double2 u2 = cmul(cadd(x2, t3), tw.at(s + 2, q, inverse));
+      const double2 u3 = cmul(csub(x2, t3), tw.at(s + 2, q + m, inverse));
+      x[sw(base + q)] = cadd(a0, u2);
+      x[sw(base + q + 2 * m)] = csub(a0, u2);
+      x[sw(base + q + m)] = cadd(a1, u3);
+      x[sw(base + q + 3 * m)] = csub(a1, u3);
     }
     __syncthreads();
   }
   if (s < logL) {  // odd log2 L: last radix-2 stage
-    const int m = 1 << s, sh = logPtw - s - 1;
+    const int m = 1 << s;
     for (int j = threadIdx.x; j < L / 2; j += blockDim.x) {
       const int k = j & (m - 1);
       const int base = (j >> s) << (s + 1);
-      const double2 a = x[base + k];
-      const double2 b = cmul(x[base + k + m], tw_at(twd, k << sh, inverse));
-      x[base + k] = cadd(a, b);
-      x[base + k + m] = csub(a, b);
+      const double2 a = x[sw(base + k)];
+      const double2 b = cmul(x[sw(base + k + m)], tw.at(s + 1, k, inverse));
+      x[sw(base + k)] = cadd(a, b);
+      x[sw(base + k + m)] = csub(a, b);
     }
     __syncthreads();
   }
@@ -144,9 +186,9 @@ __device__ __forceinline__ void fft_dit_smem(double2* x, int L, int logL, const 
 // sharded fold (fft_shard.cuh): the same arithmetic whichever block or GPU
 // computes a row or column, so the results are bit-identical.
 // Phase R, row r: half spectrum of the real row (plan_mode: of the mirrored
-// table) -> out[0..H].  buf: P double2 of shared memory, twd: staged twiddles.
+// table) -> out[0..H].  buf: P double2 of shared memory, tw: the twiddle levels.
 __device__ __forceinline__ void fold_row_r(const FftPlan& p, const double* __restrict__ src, int r,
-                                           int plan_mode, double2* buf, const double2* twd,
+                                           int plan_mode, double2* buf, const Twiddles& tw,
                                            double2* out) {
   const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1, n = p.n, N = n + 1;
   const int rows = plan_mode ? (2 * n + 1 < P ? 2 * n + 1 : P) : N;
@@ -162,16 +204,16 @@ __device__ __forceinline__ void fold_row_r(const FftPlan& p, const double* __res
       if (c0 < rows) v0 = row[abs(c0 - n)];
       if (c1 < rows) v1 = row[abs(c1 - n)];
     }
-    buf[c] = make_double2(v0, v1);
+    buf[sw(c)] = make_double2(v0, v1);
   }
   __syncthreads();
-  fft_dif_smem(buf, H, logH, twd, logP, 0);
+  fft_dif_smem(buf, H, logH, tw, 0);
   for (int k = threadIdx.x; k <= H; k += blockDim.x) {
-    const double2 zk = buf[bitrev(k & (H - 1), logH)];
-    const double2 zm = buf[bitrev((H - k) & (H - 1), logH)];
-    const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-    const double2 o = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
-    const double2 w = k < H ? twd[k] : make_double2(-1.0, 0.0);
+    const double2 zk = buf[sw(bitrev(k & (H - 1), logH))];
+    const double2 zm = buf[sw(bitrev((H - k) & (H - 1), logH))];
+    const double2 e = make_double2(half_(__dadd_rn(zk.x, zm.x)), half_(__dsub_rn(zk.y, zm.y)));
+    const double2 o = make_double2(half_(__dadd_rn(zk.y, zm.y)), -half_(__dsub_rn(zk.x, zm.x)));
+    const double2 w = k < H ? tw.top[k] : make_double2(-1.0, 0.0);
     out[k] = cadd(e, cmul(w, o));
   }
   __syncthreads();
@@ -179,24 +221,24 @@ __device__ __forceinline__ void fold_row_r(const FftPlan& p, const double* __res
 
 // Phase C, column k: load W[.][k] (rows >= `rows` zero), forward FFT; plan
 // mode stores the spectrum in KT, else multiplies by it, inverse FFT and
-// leaves the N output rows n..2n (wrapped) in buf[wrap(m)] for the caller.
+// leaves the N output rows n..2n (wrapped) in buf[sw(wrap(m))] for the caller.
 __device__ __forceinline__ void fold_col_c(const FftPlan& p, const double2* __restrict__ Wsrc,
                                            int k, int rows, int plan_mode, double2* buf,
-                                           const double2* twd) {
+                                           const Twiddles& tw) {
   const int P = p.P, logP = p.logP, ld = (P >> 1) + 1;
   for (int r = threadIdx.x; r < P; r += blockDim.x)
-    buf[r] = r < rows ? Wsrc[(size_t)r * ld + k] : make_double2(0.0, 0.0);
+    buf[sw(r)] = r < rows ? Wsrc[(size_t)r * ld + k] : make_double2(0.0, 0.0);
   __syncthreads();
-  fft_dif_smem(buf, P, logP, twd, logP, 0);
+  fft_dif_smem(buf, P, logP, tw, 0);
   double2* kt = p.KT + (size_t)k * P;
   if (plan_mode) {
-    for (int j = threadIdx.x; j < P; j += blockDim.x) kt[j] = buf[j];
+    for (int j = threadIdx.x; j < P; j += blockDim.x) kt[j] = buf[sw(j)];
     __syncthreads();
     return;
   }
-  for (int j = threadIdx.x; j < P; j += blockDim.x) buf[j] = cmul(buf[j], kt[j]);
+  for (int j = threadIdx.x; j < P; j += blockDim.x) buf[sw(j)] = cmul(buf[sw(j)], kt[j]);
   __syncthreads();
-  fft_dit_smem(buf, P, logP, twd, logP, 1);
+  fft_dit_smem(buf, P, logP, tw, 1);
 }
 __device__ __forceinline__ int fold_wrap(int m, int n, int P) {
   return m + n < P ? m + n : m + n - P;  // row 2n wraps to 0 when P = 2n
@@ -205,23 +247,23 @@ __device__ __forceinline__ int fold_wrap(int m, int n, int P) {
 // Phase I, output row m: merge the half spectrum in[0..H] and inverse FFT;
 // the N outputs are ((c & 1) ? buf[c >> 1].y : .x) * scale, c = wrap(i).
 __device__ __forceinline__ void fold_row_i(const FftPlan& p, const double2* __restrict__ in,
-                                           double2* buf, const double2* twd) {
+                                           double2* buf, const Twiddles& tw) {
   const int P = p.P, logP = p.logP, H = P >> 1, logH = logP - 1;
   for (int k = threadIdx.x; k < H; k += blockDim.x) {
     const double2 yk = in[k], ym = in[H - k];
-    const double2 e = make_double2(0.5 * (yk.x + ym.x), 0.5 * (yk.y - ym.y));
-    const double2 o = cmul(make_double2(0.5 * (yk.x - ym.x), 0.5 * (yk.y + ym.y)),
-                           tw_at(twd, k, 1));
-    buf[bitrev(k, logH)] = make_double2(e.x - o.y, e.y + o.x);
+    const double2 e = make_double2(half_(__dadd_rn(yk.x, ym.x)), half_(__dsub_rn(yk.y, ym.y)));
+    const double2 o = cmul(make_double2(half_(__dsub_rn(yk.x, ym.x)), half_(__dadd_rn(yk.y, ym.y))),
+                           tw.at(tw.logP, k, 1));
+    buf[sw(bitrev(k, logH))] = make_double2(__dsub_rn(e.x, o.y), __dadd_rn(e.y, o.x));
   }
   __syncthreads();
-  fft_dit_smem(buf, H, logH, twd, logP, 1);
+  fft_dit_smem(buf, H, logH, tw, 1);
 }
 __device__ __forceinline__ double fold_out(const double2* buf, int i, int n, int P,
                                            double scale) {
   const int c = fold_wrap(i, n, P);
-  const double2 v = buf[c >> 1];
-  return ((c & 1) ? v.y : v.x) * scale;
+  const double2 v = buf[sw(c >> 1)];
+  return __dmul_rn((c & 1) ? v.y : v.x, scale);
 }
 
 // plan_mode 0: D = deformation(src = u, N x N), gated; clears the gate and the
@@ -238,20 +280,21 @@ __global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* 
   const int ld = H + 1;
   double2* buf = fsm;
   double2* twd = fsm + P;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) twd[k] = p.tw[k];
+  twiddle_levels(twd, p.tw, p.logP);
+  const Twiddles tw{twd, p.tw, p.logP};
   const int rows = plan_mode ? (2 * n + 1 < P ? 2 * n + 1 : P) : N;
 
   // ---- R: half spectra of the real rows
   for (int r = blockIdx.x; r < rows; r += gridDim.x)
-    fold_row_r(p, src, r, plan_mode, buf, twd, p.W + (size_t)r * ld);
+    fold_row_r(p, src, r, plan_mode, buf, tw, p.W + (size_t)r * ld);
   grid.sync();
 
   // ---- C: column transforms, kernel product, inverse, output rows
   for (int k = blockIdx.x; k <= H; k += gridDim.x) {
-    fold_col_c(p, p.W, k, rows, plan_mode, buf, twd);
+    fold_col_c(p, p.W, k, rows, plan_mode, buf, tw);
     if (plan_mode) continue;
     for (int m = threadIdx.x; m < N; m += blockDim.x)
-      p.W[(size_t)m * ld + k] = buf[fold_wrap(m, n, P)];
+      p.W[(size_t)m * ld + k] = buf[sw(fold_wrap(m, n, P))];
     __syncthreads();
   }
   if (plan_mode) return;
@@ -260,7 +303,7 @@ __global__ void __launch_bounds__(256) fft_conv_kernel(FftPlan p, const double* 
   // ---- I: real output rows from their half spectra
   const double scale = 1.0 / ((double)P * (double)H);
   for (int m = blockIdx.x; m < N; m += gridDim.x) {
-    fold_row_i(p, p.W + (size_t)m * ld, buf, twd);
+    fold_row_i(p, p.W + (size_t)m * ld, buf, tw);
     double* out = D + (size_t)m * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) out[i] = fold_out(buf, i, n, P, scale);
     __syncthreads();

@@ -56,11 +56,13 @@ __global__ void __launch_bounds__(256) fold_shard_r_kernel(FftPlan p, const doub
   const int P = p.P, H = P >> 1, N = p.n + 1, ld = H + 1;
   double2* buf = fsm;
   double2* twd = fsm + P;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) twd[k] = p.tw[k];
+  twiddle_levels(twd, p.tw, p.logP);
+  const Twiddles tw{twd, p.tw, p.logP};
+  __syncthreads();
   const int lo = fold_slab_lo(N, vrank, q.world), hi = fold_slab_lo(N, vrank + 1, q.world);
   double2* own = q.W[q.rank];
   for (int r = lo + blockIdx.x; r < hi; r += gridDim.x) {
-    fold_row_r(p, u, r, 0, buf, twd, own + (size_t)r * ld);
+    fold_row_r(p, u, r, 0, buf, tw, own + (size_t)r * ld);
     for (int pr = 0; pr < q.world; ++pr) {
       if (q.W[pr] == own) continue;
       double2* dst = q.W[pr] + (size_t)r * ld;
@@ -78,13 +80,15 @@ __global__ void __launch_bounds__(256) fold_shard_c_kernel(FftPlan p, FoldPeers 
   const int P = p.P, H = P >> 1, n = p.n, N = n + 1, ld = H + 1;
   double2* buf = fsm;
   double2* twd = fsm + P;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) twd[k] = p.tw[k];
+  twiddle_levels(twd, p.tw, p.logP);
+  const Twiddles tw{twd, p.tw, p.logP};
+  __syncthreads();
   const int lo = fold_slab_lo(H + 1, vrank, q.world), hi = fold_slab_lo(H + 1, vrank + 1, q.world);
   for (int k = lo + blockIdx.x; k < hi; k += gridDim.x) {
-    fold_col_c(p, q.W[q.rank], k, N, 0, buf, twd);
+    fold_col_c(p, q.W[q.rank], k, N, 0, buf, tw);
     for (int pr = 0; pr < q.world; ++pr)
       for (int m = threadIdx.x; m < N; m += blockDim.x)
-        q.W[pr][(size_t)m * ld + k] = buf[fold_wrap(m, n, P)];
+        q.W[pr][(size_t)m * ld + k] = buf[sw(fold_wrap(m, n, P))];
     __syncthreads();
   }
   __threadfence_system();
@@ -98,11 +102,13 @@ __global__ void __launch_bounds__(256) fold_shard_i_kernel(FftPlan p, FoldPeers 
   const int P = p.P, H = P >> 1, n = p.n, N = n + 1, ld = H + 1;
   double2* buf = fsm;
   double2* twd = fsm + P;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) twd[k] = p.tw[k];
+  twiddle_levels(twd, p.tw, p.logP);
+  const Twiddles tw{twd, p.tw, p.logP};
+  __syncthreads();
   const double scale = 1.0 / ((double)P * (double)H);
   const int lo = fold_slab_lo(N, vrank, q.world), hi = fold_slab_lo(N, vrank + 1, q.world);
   for (int m = lo + blockIdx.x; m < hi; m += gridDim.x) {
-    fold_row_i(p, q.W[q.rank] + (size_t)m * ld, buf, twd);
+    fold_row_i(p, q.W[q.rank] + (size_t)m * ld, buf, tw);
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const double v = fold_out(buf, i, n, P, scale);
       for (int pr = 0; pr < q.world; ++pr) q.D[pr][(size_t)m * N + i] = v;
