@@ -158,10 +158,13 @@ __global__ void __launch_bounds__(kEhlThreads)
 ehl_line_residual_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                          const double* __restrict__ p_hertz, const double* __restrict__ lamv,
                          const double* u_in, const double* h0_in, double* film_out,
-                         double* res_out) {
-  extern __shared__ __align__(16) double esm[];
+                         double* res_out, double* gscratch, size_t gstride) {
+  extern __shared__ __align__(16) double dsm[];
   const int64_t b = blockIdx.x;
   if (b >= B) return;
+  // arrays in HBM (gscratch, one stride per case) when the grid is too fine
+  // for one CTA's shared memory
+  double* esm = gscratch ? gscratch + (size_t)b * gstride : dsm;
   const int n = c.n, N = n + 1;
   const EhlSmemLayout L(n);
   double* ext = esm + L.ext;
@@ -527,25 +530,6 @@ ehl_line_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ tabl
 // bit-identical to aqif2 in exact mode, tools/aqif2_check.cu).
 constexpr int kRungs = 4;
 
-struct SplitLayout {  // per-case workspace, offsets in doubles
-  int n_sys, s;
-  size_t band, rhs, x, zs, eps, ints, total;
-  __host__ __device__ explicit SplitLayout(int n) {
-    const int n_int = n - 1;
-    n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
-    s = n_sys / 2;
-    size_t o = 0;
-    band = o; o += (size_t)kRungs * 5 * n_sys;
-    rhs = o; o += n_sys;
-    x = o; o += (size_t)kRungs * n_sys;
-    zs = o; o += (size_t)kRungs * (s + 1) * PivotLayout<2>::kSize;
-    eps = o; o += (size_t)n + 1;
-    o = (o + 1) & ~(size_t)1;
-    ints = o; o += 4;  // status[kRungs] (int32), weighted rows (int32)
-    total = (o + 31) & ~(size_t)31;
-  }
-};
-
 struct SplitSmemA {  // phase-A kernel, offsets in doubles
   int ext, su, def, rho, eps, q, php, phm, res, red, total;
   __host__ __device__ explicit SplitSmemA(int n) {
@@ -570,13 +554,41 @@ struct SplitSmemC {  // phase-C kernel
   }
 };
 
+struct SplitLayout {  // per-case workspace, offsets in doubles
+  int n_sys, s;
+  bool gsm;
+  size_t band, rhs, x, zs, eps, ints, scratch, total;
+  __host__ __device__ explicit SplitLayout(int n) {
+    const int n_int = n - 1;
+    n_sys = (n_int + 1) % 2 == 0 ? n_int + 1 : n_int + 2;
+    s = n_sys / 2;
+    size_t o = 0;
+    band = o; o += (size_t)kRungs * 5 * n_sys;
+    rhs = o; o += n_sys;
+    x = o; o += (size_t)kRungs * n_sys;
+    zs = o; o += (size_t)kRungs * (s + 1) * PivotLayout<2>::kSize;
+    eps = o; o += (size_t)n + 1;
+    o = (o + 1) & ~(size_t)1;
+    ints = o; o += 4;  // status[kRungs] (int32), weighted rows (int32)
+    // phase A / C arrays in HBM when they do not fit one CTA's shared
+    // memory (very fine line grids: the reference has no size limit)
+    const size_t ta = SplitSmemA(n).total, tc = SplitSmemC(n).total;
+    const size_t tmax = ta > tc ? ta : tc;
+    gsm = tmax * 8 > 227 * 1024;
+    o = (o + 31) & ~(size_t)31;
+    scratch = o;
+    if (gsm) o += tmax;
+    total = (o + 31) & ~(size_t)31;
+  }
+};
+
 __global__ void __launch_bounds__(kEhlThreads)
 line_split_a_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                     const double* __restrict__ p_hertz, const double* __restrict__ lamv,
                     const double* __restrict__ u_io, const double* __restrict__ h0_io, double* ws,
                     size_t ws_per_case, const paqif_ehl_line_drive* drv)
 {
-  extern __shared__ __align__(16) double esm[];
+  extern __shared__ __align__(16) double dsm[];
   const int64_t b = blockIdx.x;
   if (b >= B || (drv && drv[b].done)) return;
   const int n = c.n, N = n + 1, n_int = n - 1;
@@ -584,6 +596,7 @@ line_split_a_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ 
   const SplitLayout W(n);
   const int n_sys = W.n_sys;
   double* w = ws + (size_t)b * ws_per_case;
+  double* esm = W.gsm ? w + W.scratch : dsm;
   double* su = esm + L.su;
   for (int k = threadIdx.x; k < N; k += blockDim.x) su[k] = u_io[b * N + k];
   ext4_build(table, n, esm + L.ext);
@@ -704,10 +717,10 @@ __global__ void __launch_bounds__(kEhlThreads)
 line_split_c_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ table,
                     const double* __restrict__ p_hertz, const double* __restrict__ lamv,
                     double* u_io, double* h0_io, double* film_out, double* res_out,
-                    double* deficit_out, int32_t* info_out, const double* ws, size_t ws_per_case,
+                    double* deficit_out, int32_t* info_out, double* ws, size_t ws_per_case,
                     paqif_ehl_line_drive* drv, double* hist_res, double* hist_def, int hist_cap)
 {
-  extern __shared__ __align__(16) double esm[];
+  extern __shared__ __align__(16) double dsm[];
   const int64_t b = blockIdx.x;
   if (b >= B) return;
   int outer = c.outer;
@@ -718,7 +731,8 @@ line_split_c_kernel(paqif_ehl_line_cfg c, int64_t B, const double* __restrict__ 
   const int n = c.n, N = n + 1;
   const SplitSmemC L(n);
   const SplitLayout W(n);
-  const double* w = ws + (size_t)b * ws_per_case;
+  double* w = ws + (size_t)b * ws_per_case;
+  double* esm = W.gsm ? w + W.scratch : dsm;
   const int32_t* wi = reinterpret_cast<const int32_t*>(w + W.ints);
   int r = 0;
   while (r < kRungs && wi[r] != 0) ++r;
@@ -808,7 +822,7 @@ int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const d
   if (workspace_bytes < need) return set_arg_error("ehl_line: workspace too small");
   const EhlSmemLayout L(cfg->n);
   const size_t smem = (size_t)L.total * 8;
-  if (smem > 227 * 1024) return set_arg_error("ehl_line: grid too fine for one CTA");
+  const bool fused_fits = smem <= 227 * 1024;  // else the split path (any n)
   const size_t per = line_ws_per_case(cfg->n) > split_ws_per_case(cfg->n)
                          ? line_ws_per_case(cfg->n) : split_ws_per_case(cfg->n);
   int32_t* order = reinterpret_cast<int32_t*>((char*)workspace + (size_t)B * per);
@@ -820,13 +834,19 @@ int line_launch(const paqif_ehl_line_cfg* cfg, int64_t B, int32_t steps, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const bool split = (flags & PAQIF_FLAG_LINE_SPLIT) ||
+  if ((flags & PAQIF_FLAG_LINE_FUSED) && !fused_fits)
+    return set_arg_error("ehl_line: grid too fine for the fused path (one CTA per case)");
+  const bool split = (flags & PAQIF_FLAG_LINE_SPLIT) || !fused_fits ||
                      (!(flags & PAQIF_FLAG_LINE_FUSED) && B >= 2 * (int64_t)sms);
   if (split) {
     const bool exact = flags & PAQIF_FLAG_EXACT;
-    const size_t sa = (size_t)SplitSmemA(cfg->n).total * 8, sc = (size_t)SplitSmemC(cfg->n).total * 8;
-    cudaFuncSetAttribute(line_split_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
-    cudaFuncSetAttribute(line_split_c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+    const bool gsm = SplitLayout(cfg->n).gsm;
+    const size_t sa = gsm ? 0 : (size_t)SplitSmemA(cfg->n).total * 8;
+    const size_t sc = gsm ? 0 : (size_t)SplitSmemC(cfg->n).total * 8;
+    if (!gsm) {
+      cudaFuncSetAttribute(line_split_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
+      cudaFuncSetAttribute(line_split_c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+    }
     static int pw = 0;
     if (!pw) {
       const char* e = getenv("PAQIF_SPLIT_PW");  // dev knob: systems per warp
@@ -896,10 +916,11 @@ extern "C" int paqif_ehl_line_drive_steps(const paqif_ehl_line_cfg* cfg, int64_t
 namespace paqif {
 __global__ void __launch_bounds__(kEhlThreads)
 line_deformation_kernel(int n, const double* __restrict__ table, const double* __restrict__ u,
-                        double* out)
+                        double* out, double* gscratch, size_t gstride)
 {
-  extern __shared__ __align__(16) double dsm[];
+  extern __shared__ __align__(16) double dsm_[];
   const int N = n + 1;
+  double* dsm = gscratch ? gscratch + (size_t)blockIdx.x * gstride : dsm_;
   double* ext = dsm;
   double* su = dsm + ext4_doubles(n);
   ext4_build(table, n, ext);
@@ -915,9 +936,18 @@ extern "C" int paqif_line_deformation(int64_t B, int64_t n, const double* table,
   if (B < 0 || n < 1) return set_arg_error("line_deformation: bad sizes");
   if (B == 0) return PAQIF_OK;
   const size_t smem = (size_t)(ext4_doubles((int)n) + n + 1 + 8) * 8;
-  if (smem > 227 * 1024) return set_arg_error("line_deformation: grid too fine");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 227 * 1024) {  // too fine for shared memory: the arrays in HBM
+    const size_t stride = ((smem / 8) + 31) & ~(size_t)31;
+    double* g = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&g, (size_t)B * stride * 8, st);
+    if (e != cudaSuccess) return set_cuda_error("line_deformation: scratch", e);
+    line_deformation_kernel<<<(unsigned)B, kEhlThreads, 0, st>>>((int)n, table, u, out, g, stride);
+    cudaFreeAsync(g, st);
+    return check_launch("paqif_line_deformation");
+  }
   cudaFuncSetAttribute(line_deformation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  line_deformation_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>((int)n, table, u, out);
+  line_deformation_kernel<<<(unsigned)B, kEhlThreads, smem, st>>>((int)n, table, u, out, nullptr, 0);
   return check_launch("paqif_line_deformation");
 }
 
@@ -929,11 +959,21 @@ extern "C" int paqif_ehl_line_residual(const paqif_ehl_line_cfg* cfg, int64_t B,
   if (!cfg || B < 0 || cfg->n < 4 || !res) return set_arg_error("ehl_line_residual: bad args");
   if (B == 0) return PAQIF_OK;
   const EhlSmemLayout L(cfg->n);
-  const size_t smem = (size_t)L.total * 8;
-  if (smem > 227 * 1024) return set_arg_error("ehl_line_residual: grid too fine for one CTA");
+  const size_t smem = (size_t)L.band * 8;  // the arrays; no line system here
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 227 * 1024) {  // too fine for shared memory: the arrays in HBM
+    const size_t stride = ((size_t)L.band + 31) & ~(size_t)31;
+    double* g = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&g, (size_t)B * stride * 8, st);
+    if (e != cudaSuccess) return set_cuda_error("ehl_line_residual: scratch", e);
+    ehl_line_residual_kernel<<<(unsigned)B, kEhlThreads, 0, st>>>(*cfg, B, table, p_hertz, lam,
+                                                                   u, h0, film, res, g, stride);
+    cudaFreeAsync(g, st);
+    return check_launch("paqif_ehl_line_residual");
+  }
   cudaFuncSetAttribute(ehl_line_residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
-  ehl_line_residual_kernel<<<(unsigned)B, kEhlThreads, smem, (cudaStream_t)stream>>>(
-      *cfg, B, table, p_hertz, lam, u, h0, film, res);
+  ehl_line_residual_kernel<<<(unsigned)B, kEhlThreads, smem, st>>>(
+      *cfg, B, table, p_hertz, lam, u, h0, film, res, nullptr, 0);
   return check_launch("paqif_ehl_line_residual");
 }

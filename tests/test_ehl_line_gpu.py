@@ -283,3 +283,57 @@ def test_split_path_device_driver():
     (d0, h0), (d1, h1) = recs
     assert np.array_equal(d0["done"], d1["done"]) and np.array_equal(d0["outer"], d1["outer"])
     np.testing.assert_allclose(h1[:, :12], h0[:, :12], rtol=1e-7)
+
+
+GB = load_golden("ehl_line_big.npz")
+BIG = sorted({k.split("__")[0] for k in GB.files}, key=lambda s: int(s[1:]))
+
+
+@pytest.mark.parametrize("key", BIG)
+@pytest.mark.parametrize("exact", [True, False])
+def test_fine_grid_single_step_vs_reference(key, exact):
+    """Line contacts finer than one CTA's shared memory (n = 4096 / 8192
+    intervals; the reference has no size limit): the split path with its
+    phase arrays in HBM, teacher-forced against the reference
+    (tests/golden/make_golden_line_big.py), incl. a ladder state."""
+    d = {k.split("__", 1)[1]: GB[k] for k in GB.files if k.startswith(key + "__")}
+    p = params_for(d)
+    n, k = int(d["meta"][2]), int(d["meta"][3])
+    u, h0, film, res, _, info = run_step([p], n, d["u_in"][None], [float(d["h0_in"])], k, exact)
+    check_against(d, u[0], h0[0], film[0], res[0], int(info[0]))
+
+
+def test_fine_grid_residual_and_deformation(rng):
+    """complementarity_residual and the line deformation past the shared-
+    memory size (arrays in HBM)."""
+    from paper_2008_03276_b200.ehl import kernel_line, line_deformation, solver
+    d = {k.split("__", 1)[1]: GB[k] for k in GB.files if k.startswith(BIG[-1] + "__")}
+    p = params_for(d)
+    n = int(d["meta"][2])
+    st = solver._initial_state(p, n)
+    st.u = d["u_out"].copy()
+    st.h0 = float(d["h0_out"])
+    assert math.isclose(st.complementarity_residual(p, 1.0 / 3.0, "kappa"), float(d["res_out"]),
+                        rel_tol=TOL)
+    m = 9000
+    t = kernel_line(m, 6.0 / m).table
+    u = np.abs(rng.standard_normal((2, m + 1)))
+    ext = np.concatenate([t[::-1], t[1:]])
+    ref = np.stack([-(1.0 / np.pi) * np.convolve(x, ext)[m:2 * m + 1] for x in u])
+    got = line_deformation(t, u)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_fine_grid_solve_ehl_device_loop():
+    """solve_ehl at n = 4096 runs on the device loop like the coarse grids:
+    same histories with and without the host loop."""
+    from paper_2008_03276_b200.ehl import solve_ehl
+    from paper_2008_03276_b200.errors import NonConvergenceError
+    p = _line_params()
+    hists = []
+    for collect in (None, lambda st, r, dd: None):
+        try:
+            solve_ehl(p, 4096, max_outer=6, collect=collect)
+        except NonConvergenceError as e:
+            hists.append((e.iterations, e.residual))
+    assert len(hists) == 2 and hists[0] == hists[1]
