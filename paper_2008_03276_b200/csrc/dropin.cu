@@ -37,7 +37,7 @@ struct DropinPol {
     return band + (size_t)(d + BETA) * n + i;
   }
   __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
-  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
+  __device__ __forceinline__ const uint64_t* pin_ptr(int) const { return nullptr; }
   __device__ __forceinline__ bool pinned(int) const { return false; }
   __device__ __forceinline__ const double* frhs_ptr(int) const { return nullptr; }
   __device__ __forceinline__ double frhs(int) const { return 0.0; }

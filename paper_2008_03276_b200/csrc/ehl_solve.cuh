@@ -26,7 +26,7 @@ struct LineSysPol {
     return band + (size_t)(d + kLineBeta) * n + i;
   }
   __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
-  __device__ __forceinline__ const uint32_t* pin_ptr(int) const { return nullptr; }
+  __device__ __forceinline__ const uint64_t* pin_ptr(int) const { return nullptr; }
   __device__ __forceinline__ bool pinned(int) const { return false; }
   __device__ __forceinline__ const double* frhs_ptr(int i) const { return rhs + i; }
   __device__ __forceinline__ double frhs(int i) const { return rhs[i]; }

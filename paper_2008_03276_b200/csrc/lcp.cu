@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <mutex>
 #include "aqif_warp.cuh"
+#include "aqif_pipe.cuh"
 #include "zsolve.cuh"
 #include "capi_util.cuh"
 
@@ -35,10 +36,13 @@ struct LcpPol {
   static constexpr bool kResidual = false;
   static constexpr bool kFastDiv = true;  // branch-free divisions, checked repeat
   static constexpr bool kLazyBreakdown = true;  // breakdown found after the loop
+  // ... and not even tested in the loop: the Z solve and the corner system
+  // read every pivot record and apply the level test there
+  static constexpr bool kDeferBreakdown = true;
   static constexpr bool kRecordW = false;
   using PL = PivotLayout<BETA>;
   const double* band;
-  const uint32_t* act;
+  const uint64_t* act;
   const double* f;
   double* zs;
   int n;
@@ -48,12 +52,16 @@ struct LcpPol {
     return band + (size_t)(d + BETA) * n + i;
   }
   __device__ __forceinline__ double raw(int i, int d) const { return *raw_ptr(i, d); }
-  __device__ __forceinline__ const uint32_t* pin_ptr(int i) const {
+  __device__ __forceinline__ const uint64_t* pin_ptr(int i) const {
     return use_act ? act + i : nullptr;
   }
-  __device__ __forceinline__ bool pinned(int i) const { return use_act && act[i] != 0u; }
+  __device__ __forceinline__ bool pinned(int i) const { return use_act && act[i] != 0ull; }
   __device__ __forceinline__ const double* frhs_ptr(int i) const { return f + i; }
   __device__ __forceinline__ double frhs(int i) const { return f[i]; }
+  // level k's pivot record (pivot rows + W-solved right sides, 38 doubles at
+  // BETA = 8) to the Z stack, copied from the pivot buffer by the group's
+  // lanes (16-byte coalesced stores)
+  __device__ __forceinline__ double* record_out(int k) const { return zs + (size_t)k * PL::kSize; }
   __device__ __forceinline__ void on_level(int k, const double* pb, int gl, int G) {
     double2* dst = reinterpret_cast<double2*>(zs + (size_t)k * PL::kSize);
     const double2* src = reinterpret_cast<const double2*>(pb);
@@ -64,6 +72,9 @@ struct LcpPol {
       if (idx < NP) dst[idx] = src[idx];
     }
   }
+  // all records in global memory before the corner system / Z solve read
+  // them (the warp barrier orders the lanes' stores); all lanes call
+  __device__ __forceinline__ void records_done(int) { __syncwarp(); }
   __device__ __forceinline__ void on_w(int, int, double, double) {}
   __device__ __forceinline__ void on_resid(int, int, double) {}
   __device__ __forceinline__ const double* record(int k) const { return zs + (size_t)k * PL::kSize; }
@@ -115,8 +126,13 @@ struct LcpSmem {
 // solved through R^T R Cholesky as solve_reduced does (parallel.py:227-231).
 // Runs on the G lanes of the system's group; all 32 lanes call (syncs).
 // Returns 0 or 1 (not SPD).
+// Also applies the factorization's level test (_kernels.py:112-122; the
+// LCP policy defers it) to the outermost levels s-BETA+1 .. s-1, whose
+// records only the corner system reads: `fbad` = the smallest failing
+// level there, or 0 (group-uniform).
 template <int BETA, bool EXACT>
-__device__ int corner_solve(const double* zs, int n, double* x, double* cs, int gl, bool alive)
+__device__ int corner_solve(const double* zs, int n, double* x, double* cs, int gl, bool alive,
+                            int& fbad)
 {
   using A = Arith<EXACT>;
   using PL = PivotLayout<BETA>;
@@ -127,6 +143,24 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
   double* rtr = rd + m * m;
   double* fd = rtr + m * m;
   double* rtf = fd + m;
+  {
+    int lv = 0;
+    if (alive && gl < BETA - 1) {
+      const int k = s - BETA + 1 + gl;
+      const double* rec = zs + (size_t)k * PL::kSize;
+      const double a11 = rec[PL::zi(0, 0, 0)], a12 = rec[PL::zi(1, 0, 0)];
+      const double a21 = rec[PL::zi(0, 0, 1)], a22 = rec[PL::zi(1, 0, 1)];
+      const double det = A::det2(a11, a22, a21, a12);
+      const double scale = fmax(fmax(fabs(a11), fabs(a12)), fmax(fabs(a21), fabs(a22)));
+      lv = fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY ? k : 0;
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const int w = __shfl_xor_sync(0xffffffffu, lv, o);
+      lv = (lv == 0 || (w != 0 && w < lv)) ? w : lv;
+    }
+    fbad = lv;
+  }
   if (alive)
     for (int idx = gl; idx < m * m; idx += G) rd[idx] = 0.0;
   __syncwarp();
@@ -236,9 +270,11 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
   size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
   double* x = reinterpret_cast<double*>(my + off);
   off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
-  uint32_t* act = reinterpret_cast<uint32_t*>(my + off);
-  off += ((size_t)n * 4 + 255) & ~(size_t)255;
-  uint32_t* nact = reinterpret_cast<uint32_t*>(my + off);
+  // active sets as 64-bit words: the factorization copies the flags with
+  // the band values (8-byte cp.async)
+  uint64_t* act = reinterpret_cast<uint64_t*>(my + off);
+  off += ((size_t)n * 8 + 255) & ~(size_t)255;
+  uint64_t* nact = reinterpret_cast<uint64_t*>(my + off);
 #ifdef PAQIF_PROFILE_PHASES
   unsigned long long ph_acc[4] = {0, 0, 0, 0};
 #endif
@@ -254,13 +290,22 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
     double* ub = u_out + (have ? b : 0) * (size_t)n;
     uint8_t* ab = SOLVE_ONLY ? nullptr : act_out + (have ? b : 0) * (size_t)n;
     if (have) {
-      for (int i = gl; i < n; i += G) {
-        const double fi = fb[i];
-        const uint32_t a = SOLVE_ONLY ? 0u : (fi <= 0.0 ? 1u : 0u);
-        act[i] = a;
-        if (!SOLVE_ONLY) {
-          ub[i] = 0.0;
-          ab[i] = (uint8_t)a;
+      // initial policy active = f <= 0 (parallel.py:312); four loads of f in
+      // flight per lane
+      for (int i0 = gl; i0 < n; i0 += 4 * G) {
+        double fv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) fv[u] = i0 + u * G < n ? __ldg(fb + i0 + u * G) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * G;
+          if (i >= n) break;
+          const uint64_t a = SOLVE_ONLY ? 0ull : (fv[u] <= 0.0 ? 1ull : 0ull);
+          act[i] = a;
+          if (!SOLVE_ONLY) {
+            ub[i] = 0.0;
+            ab[i] = (uint8_t)a;
+          }
         }
       }
     }
@@ -268,8 +313,8 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
     int passes = 0, st = 0, brk_level = 0;
     bool done = false;
     bool active = have;  // this group still iterating
-    uint32_t* cur = act;
-    uint32_t* nxt = nact;
+    uint64_t* cur = act;
+    uint64_t* nxt = nact;
     for (int outer = 0; outer < max_outer; ++outer) {
       if (!__any_sync(FULL, active)) break;
       __syncwarp();
@@ -282,7 +327,13 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       pol.use_act = !SOLVE_ONLY;
       if (active) passes = outer + 1;
       PAQIF_TSTAMP(t0);
-      int fst = aqif_factor_group<BETA, EXACT>(pol, n, 1e-14, my_sm.eng, gl, active);
+      // FMA arithmetic: the software-pipelined level loop (aqif_pipe.cuh);
+      // reference rounding: the general engine
+      int fst = 0;
+      if constexpr (EXACT)
+        fst = aqif_factor_group<BETA, EXACT>(pol, n, 1e-14, my_sm.eng, gl, active);
+      else
+        aqif_factor_pipe<BETA>(pol, n, my_sm.eng, gl, active);
       if (EXACT && __any_sync(FULL, fst < 0)) {
         // a multiplier left the branch-free division's range: repeat this
         // system's factorization with IEEE divisions (the others idle)
@@ -296,12 +347,15 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         brk_level = fst;
         active = false;
       }
-      __syncwarp();
+      pol.records_done(gl);
       PAQIF_TSTAMP(t1);
-      if (corner_solve<BETA, EXACT>(zs, n, x, my_sm.post.scratch, gl, active)) {
-        st = PAQIF_LCP_NOT_PD;
-        active = false;
-      }
+      // the factorization's breakdown test runs on the records: here for
+      // the outermost levels, in the Z solve for the rest; a breakdown
+      // outranks the corner system's failure (the reference raises in
+      // factorize_wz first, aqif.py:133-134)
+      int fbad_corner = 0;
+      const bool not_pd =
+          corner_solve<BETA, EXACT>(zs, n, x, my_sm.post.scratch, gl, active, fbad_corner) != 0;
       PAQIF_TSTAMP(t2);
       if (!SOLVE_ONLY && active) {
         // the band and f into L2 while the Z chain runs, for the
@@ -321,10 +375,19 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
                        "r"((unsigned)(n * 8))
                        : "memory");
       }
-      if (const int zst = zsolve_group<BETA, EXACT, false>(zs, n, x, my_sm.post.scratch, gl, active)) {
-        st = PAQIF_LCP_ZSOLVE_BREAKDOWN;
-        brk_level = zst;
-        active = false;
+      {
+        const int fbad_z =
+            zsolve_group<BETA, EXACT, false, Group<BETA>::G, true>(zs, n, x, my_sm.post.scratch, gl,
+                                                                   active);
+        const int fbad = fbad_z ? fbad_z : fbad_corner;
+        if (active && fbad) {
+          st = PAQIF_LCP_FACTOR_BREAKDOWN;
+          brk_level = fbad;
+          active = false;
+        } else if (active && not_pd) {
+          st = PAQIF_LCP_NOT_PD;
+          active = false;
+        }
       }
       PAQIF_TSTAMP(t3);
       PAQIF_TACC(0, t0, t1);
@@ -342,48 +405,33 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
       double r = 0.0;
       int changed = 0;
       if (active) {
-        // one row of L x and L max(x, 0) against f (interior rows: all
-        // 2*BETA+1 terms, loads issued first)
-        auto row = [&](int i) {
-          double acc1 = 0.0, acc2 = 0.0;
-          if (i >= BETA && i < n - BETA) {
-            const double* pa = bd + i;
-            const double* px = x + (i - BETA);
-            double av[2 * BETA + 1], xv[2 * BETA + 1];
-#pragma unroll
-            for (int d = 0; d <= 2 * BETA; ++d) {
-              av[d] = __ldg(pa + (size_t)d * n);
-              xv[d] = px[d];
-            }
-#pragma unroll
-            for (int d = 0; d <= 2 * BETA; ++d) {
-              acc1 = A::axpy(acc1, av[d], xv[d]);
-              acc2 = A::axpy(acc2, av[d], np_max0(xv[d]));
-            }
-          } else {
-            const int lo = i - BETA > 0 ? i - BETA : 0;
-            const int hi = i + BETA + 1 < n ? i + BETA + 1 : n;
-            for (int j = lo; j < hi; ++j) {
-              const double a = bd[(size_t)(j - i + BETA) * n + i];
-              const double xe = x[j];
-              acc1 = A::axpy(acc1, a, xe);
-              acc2 = A::axpy(acc2, a, np_max0(xe));
-            }
-          }
-          const double xi = x[i];
-          const double lam = A::sub(acc1, fb[i]);
-          const double rr = A::sub(acc2, fb[i]);
+        // one row of L x and L max(x, 0) against f, given its loads
+        auto finish = [&](int i, double acc1, double acc2, double xi, double fi, uint64_t ci) {
+          const double lam = A::sub(acc1, fi);
+          const double rr = A::sub(acc2, fi);
           const double mn = fabs(np_min(np_max0(xi), rr));
           r = ((r != r) | (mn != mn)) ? __longlong_as_double(0x7ff8000000000000ll) : (mn > r ? mn : r);
-          const uint32_t na = xi < lam ? 1u : 0u;
+          const uint64_t na = xi < lam ? 1ull : 0ull;
           nxt[i] = na;
-          changed |= (na != cur[i]);
+          changed |= (na != ci);
         };
-        // rows in order (the NaN-propagating max is order independent),
-        // two per step so twice the loads are in flight
-        // prefetch into L1 the band lines of the next step's rows (2 x 16
-        // rows x 17 diagonals = 34 lines of 128 B; about 2 per lane) so its
-        // loads hit L1 instead of waiting on DRAM
+        auto edge_row = [&](int i) {  // rows whose band runs off the matrix
+          double acc1 = 0.0, acc2 = 0.0;
+          const int lo = i - BETA > 0 ? i - BETA : 0;
+          const int hi = i + BETA + 1 < n ? i + BETA + 1 : n;
+          for (int j = lo; j < hi; ++j) {
+            const double a = bd[(size_t)(j - i + BETA) * n + i];
+            const double xe = x[j];
+            acc1 = A::axpy(acc1, a, xe);
+            acc2 = A::axpy(acc2, a, np_max0(xe));
+          }
+          finish(i, acc1, acc2, x[i], fb[i], cur[i]);
+        };
+        // interior rows two per step (i, i+G): every load of the step -- 2 x
+        // 17 band values, the x windows, f and the active flags -- issued
+        // before the first use, so a step waits for one memory round trip
+        // (the band comes from HBM here); the band lines two steps ahead are
+        // prefetched into L1
         auto prefetch_rows = [&](int r0) {
           for (int q = gl; q < 2 * (2 * BETA + 1); q += G) {
             const int d = q >> 1, rr = r0 + (q & 1) * G;
@@ -391,13 +439,46 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
               asm volatile("prefetch.global.L1 [%0];" ::"l"(bd + (size_t)d * n + rr));
           }
         };
+        constexpr int ND = 2 * BETA + 1;
         int i = gl;
-        for (; i + G < n; i += 2 * G) {
+        for (; i < BETA; i += G) edge_row(i);  // G >= BETA: at most one
+        for (; i + G < n - BETA; i += 2 * G) {
           prefetch_rows(i - gl + 4 * G);
-          row(i);
-          row(i + G);
+          double av0[ND], xv0[ND], av1[ND], xv1[ND];
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            av0[d] = __ldg(bd + (size_t)d * n + i);
+            av1[d] = __ldg(bd + (size_t)d * n + i + G);
+            xv0[d] = x[i - BETA + d];
+            xv1[d] = x[i + G - BETA + d];
+          }
+          const double f0 = __ldg(fb + i), f1 = __ldg(fb + i + G);
+          const uint64_t c0 = cur[i], c1 = cur[i + G];
+          double p0 = 0.0, q0 = 0.0, p1 = 0.0, q1 = 0.0;
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            p0 = A::axpy(p0, av0[d], xv0[d]);
+            q0 = A::axpy(q0, av0[d], np_max0(xv0[d]));
+            p1 = A::axpy(p1, av1[d], xv1[d]);
+            q1 = A::axpy(q1, av1[d], np_max0(xv1[d]));
+          }
+          finish(i, p0, q0, xv0[BETA], f0, c0);
+          finish(i + G, p1, q1, xv1[BETA], f1, c1);
         }
-        if (i < n) row(i);
+        for (; i < n; i += G) {
+          if (i >= BETA && i < n - BETA) {
+            double acc1 = 0.0, acc2 = 0.0;
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+              const double a = __ldg(bd + (size_t)d * n + i), xe = x[i - BETA + d];
+              acc1 = A::axpy(acc1, a, xe);
+              acc2 = A::axpy(acc2, a, np_max0(xe));
+            }
+            finish(i, acc1, acc2, x[i], fb[i], cur[i]);
+          } else {
+            edge_row(i);
+          }
+        }
       }
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) {
@@ -413,7 +494,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         int i = gl;
         for (; i + 3 * G < n; i += 4 * G) {  // loads of four rows in flight
           const double x0 = x[i], x1 = x[i + G], x2 = x[i + 2 * G], x3 = x[i + 3 * G];
-          const uint32_t c0 = cur[i], c1 = cur[i + G], c2 = cur[i + 2 * G], c3 = cur[i + 3 * G];
+          const uint64_t c0 = cur[i], c1 = cur[i + G], c2 = cur[i + 2 * G], c3 = cur[i + 3 * G];
           ub[i] = np_max0(x0);
           ub[i + G] = np_max0(x1);
           ub[i + 2 * G] = np_max0(x2);
@@ -438,7 +519,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         active = false;
         continue;
       }
-      uint32_t* t = cur;
+      uint64_t* t = cur;
       cur = nxt;
       nxt = t;
     }
@@ -495,8 +576,8 @@ size_t lcp_ws_per_slot(int n) {
   const int s = n / 2;
   size_t off = (((size_t)(s + 1) * PL::kSize * sizeof(double)) + 255) & ~(size_t)255;
   off += (((size_t)n * sizeof(double)) + 255) & ~(size_t)255;
-  off += ((size_t)n * 4 + 255) & ~(size_t)255;
-  off += ((size_t)n * 4 + 255) & ~(size_t)255;
+  off += ((size_t)n * 8 + 255) & ~(size_t)255;
+  off += ((size_t)n * 8 + 255) & ~(size_t)255;
   return off;
 }
 

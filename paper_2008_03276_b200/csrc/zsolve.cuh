@@ -90,14 +90,77 @@ __device__ __forceinline__ bool zlevel(const double* rec, int sd, int p, int n, 
   return !bad;
 }
 
+// FMA arithmetic, both rows of a level in one lane: the two chain lanes
+// compute the same pair (no shuffle on the level chain).  Per row the same
+// expressions as zlevel's FMA branch; the record's (top, bottom) entries of
+// one column are adjacent, so each 16-byte load serves both rows.
+template <int BETA, bool CHECK>
+__device__ __forceinline__ bool zlevel_fma2(const double* rec, int p, int n, double& xp,
+                                            double& xq, const double* xl, const double* xr,
+                                            int ph)
+{
+  using A = Arith<false>;
+  using PL = PivotLayout<BETA>;
+  const int q = n - 1 - p;
+  const double2* r2 = reinterpret_cast<const double2*>(rec);
+  const double2 c0 = r2[PL::zi(0, 0, 0) / 2];  // (a11, a21)
+  const double2 c1 = r2[PL::zi(1, 0, 0) / 2];  // (a12, a22)
+  const double a11 = c0.x, a21 = c0.y, a12 = c1.x, a22 = c1.y;
+  const double det = A::det2(a11, a22, a12, a21);
+  double scale = fabs(a11);
+  if (fabs(a12) > scale) scale = fabs(a12);
+  if (fabs(a21) > scale) scale = fabs(a21);
+  if (fabs(a22) > scale) scale = fabs(a22);
+  const bool bad = fabs(det) <= 1e-14 * (scale * scale) + PAQIF_TINY;
+  // branch-free: a det outside the normal range fails the test above
+  const double y = rcp_nobranch(det);
+  const double2 yy = r2[PL::kYT / 2];
+  double acc_t = yy.x, acc_b = yy.y, accr_t = 0.0, accr_b = 0.0;
+#pragma unroll
+  for (int t = 0; t < BETA; ++t) {
+    if (t != BETA - 1 && (!CHECK || p - BETA + t >= 0)) {
+      const double2 z = r2[PL::zi(0, BETA - t, 0) / 2];
+      const double xv = xl[(ph + t) % BETA];
+      acc_t = A::axpy_neg(acc_t, z.x, xv);
+      acc_b = A::axpy_neg(acc_b, z.y, xv);
+    }
+    if (t != 0 && (!CHECK || q + 1 + t < n)) {
+      const double2 z = r2[PL::zi(1, 1 + t, 0) / 2];
+      const double xv = xr[(ph - 1 - t + 2 * BETA) % BETA];
+      accr_t = A::axpy_neg(accr_t, z.x, xv);
+      accr_b = A::axpy_neg(accr_b, z.y, xv);
+    }
+  }
+  acc_t = acc_t + accr_t;
+  acc_b = acc_b + accr_b;
+  if (!CHECK || q + 1 < n) {
+    const double2 z = r2[PL::zi(1, 1, 0) / 2];
+    const double xv = xr[(ph - 1 + 2 * BETA) % BETA];
+    acc_t = A::axpy_neg(acc_t, z.x, xv);
+    acc_b = A::axpy_neg(acc_b, z.y, xv);
+  }
+  if (!CHECK || p - 1 >= 0) {
+    const double2 z = r2[PL::zi(0, 1, 0) / 2];
+    const double xv = xl[(ph + BETA - 1) % BETA];
+    acc_t = A::axpy_neg(acc_t, z.x, xv);
+    acc_b = A::axpy_neg(acc_b, z.y, xv);
+  }
+  xp = fma_mult(a22, acc_t, a12, acc_b, y);
+  xq = fma_mult(a11, acc_b, a21, acc_t, y);
+  return !bad;
+}
+
 // All 32 lanes call.  Returns 0 or the 1-based breakdown level.
-template <int BETA, bool EXACT, bool FULL>
+// SCAN: the level test is the FACTORIZATION's (policies with
+// kDeferBreakdown): every level is solved (no early stop) and the return
+// value is the smallest factor level k = s - p whose pivot fails the test
+// (the Z solve's own test on the same record is the same test).
+template <int BETA, bool EXACT, bool FULL, int G = Group<BETA>::G, bool SCAN = false>
 __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, int gl, bool alive)
 {
   using PL = PivotLayout<BETA>;
   constexpr int ZC = ZChunk<BETA>::ZC;
   constexpr int RS = PL::kSize;
-  constexpr int G = Group<BETA>::G;
   const int s = n / 2;
   const int p0 = FULL ? 0 : BETA;  // first unknown pair solved
   const int M = s - p0;            // levels to solve
@@ -139,7 +202,7 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
       cp_async_wait<0>();
     }
     __syncwarp();
-    if (alive && gl < 2 && status == 0) {
+    if (alive && gl < 2 && (SCAN || status == 0)) {
       const int k_hi = s - p0 - c0;
       const int k_lo = max(1, k_hi - ZC + 1);
       const double* buf = ring + cb * ZC * RS;
@@ -149,25 +212,36 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
         if (p >= s) break;
         const double* rec = buf + (s - p - k_lo) * RS;
         double xp, xq;
-        const bool ok = (FULL && p < BETA)
-                            ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
-                            : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
-        status = (!ok & (status == 0)) ? p + 1 : status;  // first failing level, no branch
+        bool ok;
+        if constexpr (EXACT)
+          ok = (FULL && p < BETA)
+                   ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
+                   : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
+        else
+          ok = (FULL && p < BETA) ? zlevel_fma2<BETA, true>(rec, p, n, xp, xq, xl, xr, ph)
+                                  : zlevel_fma2<BETA, false>(rec, p, n, xp, xq, xl, xr, ph);
+        if (SCAN)
+          status = ok ? status : s - p;  // ascending p: the last one is the smallest level
+        else
+          status = (!ok & (status == 0)) ? p + 1 : status;  // first failing level, no branch
         x[sd == 0 ? p : n - 1 - p] = sd == 0 ? xp : xq;
         xl[ph % BETA] = xp;
         xr[ph % BETA] = xq;
       }
     }
-    // group-uniform status (lane 0 of the group holds it)
-    status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
-    if (__all_sync(0xffffffffu, status != 0 || !alive)) {
-      cp_async_wait<0>();
-      break;
+    if (!SCAN) {
+      // group-uniform status (lane 0 of the group holds it)
+      status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
+      if (__all_sync(0xffffffffu, status != 0 || !alive)) {
+        cp_async_wait<0>();
+        break;
+      }
     }
     __syncwarp();
   }
   cp_async_wait<0>();
   __syncwarp();
+  if (SCAN) status = __shfl_sync(0xffffffffu, status, (threadIdx.x & 31) & ~(G - 1));
   return status;
 }
 

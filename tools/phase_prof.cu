@@ -64,8 +64,8 @@ int main(int argc, char** argv) {
   unsigned long long sg[9];
   cudaMemcpyFromSymbol(sg, g_engine_seg, sizeof(sg));
   const double L = sg[5] ? (double)sg[5] : 1.0;
-  printf("  engine cycles/level: head(det,vote) %.0f div %.0f update %.0f hookwait %.0f shift %.0f handoff %.0f syncwarp %.0f issue %.0f (levels %llu)\n",
-         sg[0] / L, sg[1] / L, sg[2] / L, sg[3] / L, sg[4] / L, sg[6] / L, sg[7] / L, sg[8] / L, sg[5]);
+  printf("  engine cycles/level (pipe: chain, bulk, rec+hooks, hookwait, hookread, handoff, sync; row engine: head, div, update, hookwait, shift, -, handoff, syncwarp): %.0f %.0f %.0f %.0f %.0f %.0f %.0f (levels %llu)\n",
+         sg[0] / L, sg[1] / L, sg[2] / L, sg[3] / L, sg[4] / L, sg[6] / L, sg[7] / L, sg[5]);
 #endif
   return 0;
 }
