@@ -7,6 +7,11 @@ PAQIF_SHIM=kernels  sys.modules["paqif._kernels"] = paper_2008_03276_b200._kerne
                     reference's Python drives them unchanged)
 PAQIF_SHIM=fused    additionally paqif.errors -> ours and the fused entry
                     points paqif.parallel.paqif_solve / paqif_solve_lcp -> ours
+PAQIF_SHIM=tvd      kernels, plus the TVD study's sweep entry points
+                    paqif.tvdcd.sweep_splitting / solve_by_sweeps -> the device
+                    sweeps (tvd_sweep.cu) for the AQIF splittings; DefC (the
+                    sparse direct baseline, not on the device path) stays the
+                    reference's
 PAQIF_SHIM_OUT      JSON file receiving the per-entry call counts at exit
 """
 
@@ -49,6 +54,22 @@ if MODE == "fused":
     from paper_2008_03276_b200 import parallel as _ours  # noqa: E402
     _ref_parallel.paqif_solve = _counted("paqif_solve", _ours.paqif_solve)
     _ref_parallel.paqif_solve_lcp = _counted("paqif_solve_lcp", _ours.paqif_solve_lcp)
+
+if MODE == "tvd":
+    import paqif.tvdcd as _ref_tvd  # noqa: E402
+    from paper_2008_03276_b200 import tvdcd as _our_tvd  # noqa: E402
+
+    def _route(name):
+        ref_fn, dev_fn = getattr(_ref_tvd, name), _counted(name, getattr(_our_tvd, name))
+
+        def entry(problem, *a, **k):
+            variant = a[1] if name == "sweep_splitting" and len(a) > 1 else (
+                a[0] if name == "solve_by_sweeps" and a else k.get("variant"))
+            return (ref_fn if variant == "DefC" else dev_fn)(problem, *a, **k)
+        entry.__name__, entry.__doc__ = name, ref_fn.__doc__
+        return entry
+    _ref_tvd.sweep_splitting = _route("sweep_splitting")
+    _ref_tvd.solve_by_sweeps = _route("solve_by_sweeps")
 
 import paqif  # noqa: E402,F401  (binds the swapped modules now)
 assert sys.modules["paqif._kernels"] is _mod

@@ -182,3 +182,30 @@ def test_lcp_wild_systems_status_vs_oracle(beta):
     assert np.array_equal(r.active[ok], act[ok])
     assert np.array_equal(_bits(r.u[ok]), _bits(u[ok]))
     assert len(set(st.tolist())) >= 2, "the batch should mix outcomes"
+
+
+@pytest.mark.parametrize("beta", [2, 8])
+def test_lcp_wild_systems_fma_status(beta):
+    """FMA arithmetic (the pipelined factorization, which defers the level
+    test to the records the Z solve and the corner system read) on the same
+    non-dominant systems: the same outcome per system as the oracle -- the
+    same breakdown level, the same passes -- and values within 1e-9 where
+    the solve succeeds."""
+    from paper_2008_03276_b200.batch import lcp_batch
+    from paper_2008_03276_b200.workloads import lcp_batch as gen
+    rng = np.random.default_rng(77 + beta)
+    B, n = 48, 129
+    bands, f = gen(5, B, n=n, beta=beta)
+    diag = bands[:, beta, :]
+    wild = rng.random(B) < 0.5
+    diag[wild, :n] = rng.uniform(-1.0, 1.0, (int(wild.sum()), n))
+    u, act, passes, res, st = O.lcp_batch(bands, f, threads=8)
+    r = lcp_batch(bands, f, exact=False)
+    assert np.array_equal(r.status, st)
+    assert np.array_equal(r.passes, passes)
+    brk = st == 1
+    assert np.array_equal(r.res[brk], res[brk]), "breakdown levels"
+    ok = st == 0
+    assert np.array_equal(r.active[ok], act[ok])
+    scale = np.maximum(1.0, np.max(np.abs(u[ok]), axis=1, keepdims=True))
+    assert np.max(np.abs(r.u[ok] - u[ok]) / scale) <= 1e-9

@@ -1,5 +1,5 @@
 """The reference's own tests (pkg/tests: test_aqif, test_parallel, test_lcp,
-test_bandcore), unmodified, run against the device kernels through the
+test_bandcore, test_tvdcd), unmodified, run against the device kernels through the
 INTEGRATION.md binding (tests/refshim/b200_shim.py).
 
 baseline/_ref holds the unmodified reference package and its tests
@@ -53,4 +53,13 @@ def test_reference_suite_on_device_kernels(tmp_path):
 def test_reference_suite_on_fused_entries(tmp_path):
     calls, tail = _run("fused", ["test_parallel.py", "test_lcp.py"], tmp_path)
     assert calls.get("paqif_solve", 0) > 5 and calls.get("paqif_solve_lcp", 0) > 2, calls
+    print(tail.splitlines()[-1], calls)
+
+
+def test_reference_tvd_suite_on_device_sweeps(tmp_path):
+    """test_tvdcd.py (the linear TVD study: kappa operators, limiters, the
+    line-splitting sweeps) with the sweep entry points on the device sweeps
+    and every AQIF call on the device kernels."""
+    calls, tail = _run("tvd", ["test_tvdcd.py"], tmp_path)
+    assert calls.get("solve_by_sweeps", 0) > 3 and calls.get("sweep_splitting", 0) > 0, calls
     print(tail.splitlines()[-1], calls)
