@@ -153,22 +153,44 @@ __device__ void aqif_factor_pipe(Pol& pol, const int n, EngineSmem<BETA>& sm, co
     // basic block and with it the scheduler's freedom to interleave)
     const double yn = rcp_nobranch(A::det2(n11, n22, n21, n12));
     ENG_T(t1);
-    // ---- off the chain: the rest of the update, right side, record, hooks
+    // ---- this level's hooks (copied HOOK_AHEAD levels ago; the groups of
+    // the next HOOK_AHEAD-1 levels may still be in flight), read before the
+    // bulk update so their latency hides under it
+    cp_async_wait<HOOK_AHEAD - 1>();
+    __syncwarp();
+    const double* hk = sm.hooks[k & (HOOK_RING - 1)] + side * HL::kSide;
+    int m = side == 0 ? row - (rt - BETA) : (rb + BETA) - row;
+    m = m < 0 ? 0 : (m > BETA - 1 ? BETA - 1 : m);
+    const double hcol = hk[HL::kCol + m];
+    const bool npin = reinterpret_cast<const uint32_t*>(hk + HL::kPin)[0] != 0u;
+    const double nf = hk[HL::kF];
+    double nrw[BP1];
+    {
+      const double2* h2 = reinterpret_cast<const double2*>(hk + HL::kRow);
+#pragma unroll
+      for (int e = 0; e + 1 < BP1; e += 2) {
+        const double2 v = h2[e / 2];
+        nrw[e] = v.x;
+        nrw[e + 1] = v.y;
+      }
+      if (BP1 & 1) nrw[BP1 - 1] = hk[HL::kRow + BP1 - 1];
+    }
+    hp.issue(sm, k + HOOK_AHEAD);
+    cp_async_commit();
+    ENG_T(t2);
+    // ---- off the chain: the rest of the update, right side, record
 #pragma unroll
     for (int e = 2; e < BP1; ++e) {
       const double2 vo = po[e], vc = pc[e];
       wo[e - 1] = A::rank2(wo[e], w1, vo.x, w2, vo.y);
       wc[e - 1] = A::rank2(wc[e], w1, vc.x, w2, vc.y);
     }
-    ENG_T(t2);
     const double2 yy = reinterpret_cast<const double2*>(pb)[PL::kYT / 2];  // (yt, yb)
     const bool row_ok = alive & on & (row >= 0) & (row < n);
     {
       const double nr = fma_wsub(rhs, yy.x, w1, yy.y, w2);
       rhs = row_ok ? nr : rhs;
     }
-    hp.issue(sm, k + HOOK_AHEAD);
-    cp_async_commit();
 #ifndef PAQIF_DEV_NO_RECORD
     if (alive) {
       double2* dst = reinterpret_cast<double2*>(pol.record_out(k));
@@ -178,14 +200,7 @@ __device__ void aqif_factor_pipe(Pol& pol, const int n, EngineSmem<BETA>& sm, co
     }
 #endif
     ENG_T(t3);
-    // this level's hooks (copied HOOK_AHEAD levels ago)
-    cp_async_wait<HOOK_AHEAD>();
-    __syncwarp();
     ENG_T(t4);
-    const double* hk = sm.hooks[k & (HOOK_RING - 1)] + side * HL::kSide;
-    int m = side == 0 ? row - (rt - BETA) : (rb + BETA) - row;
-    m = m < 0 ? 0 : (m > BETA - 1 ? BETA - 1 : m);
-    const double hcol = hk[HL::kCol + m];
     // the column entering at distance BETA: band value in the own window,
     // anti-band fill (zero) in the cross one
     wo[BETA] = (row_ok & !cur_pin) ? hcol : 0.0;
@@ -204,18 +219,8 @@ __device__ void aqif_factor_pipe(Pol& pol, const int n, EngineSmem<BETA>& sm, co
       }
       pbn[side == 0 ? PL::kYT : PL::kYB] = rhs;
       row += step;
-      const bool npin = reinterpret_cast<const uint32_t*>(hk + HL::kPin)[0] != 0u;
       cur_pin = npin;
-      rhs = npin ? 0.0 : hk[HL::kF];
-      double nrw[BP1];
-      const double2* h2 = reinterpret_cast<const double2*>(hk + HL::kRow);
-#pragma unroll
-      for (int e = 0; e + 1 < BP1; e += 2) {
-        const double2 v = h2[e / 2];
-        nrw[e] = v.x;
-        nrw[e + 1] = v.y;
-      }
-      if (BP1 & 1) nrw[BP1 - 1] = hk[HL::kRow + BP1 - 1];
+      rhs = npin ? 0.0 : nf;
 #pragma unroll
       for (int e = 0; e < BP1; ++e) {
         wo[e] = npin ? pinned_entry(e == BETA ? 0 : 1, nrw[BETA]) : nrw[e];

@@ -432,11 +432,19 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         // before the first use, so a step waits for one memory round trip
         // (the band comes from HBM here); the band lines two steps ahead are
         // prefetched into L1
+        // (and the lines of x, f and the active flags those rows read)
         auto prefetch_rows = [&](int r0) {
           for (int q = gl; q < 2 * (2 * BETA + 1); q += G) {
             const int d = q >> 1, rr = r0 + (q & 1) * G;
             if (rr < n)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(bd + (size_t)d * n + rr));
+          }
+          if (gl < 6) {  // 2G rows: x window (3 lines), f (1-2), flags (2)
+            const int q = gl;
+            const void* pp = q < 3 ? (const void*)(x + min(max(r0 - BETA + 16 * q, 0), n - 1))
+                             : q < 4 ? (const void*)(fb + min(r0, n - 1))
+                                     : (const void*)(cur + min(r0 + 16 * (q - 4), n - 1));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pp));
           }
         };
         constexpr int ND = 2 * BETA + 1;

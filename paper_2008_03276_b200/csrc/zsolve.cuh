@@ -10,6 +10,7 @@
 //   FULL = true : solve_z(start_level = 1) -- a plain AQIF solve (the EHL
 //                 line solves, ehl/sweeps.py:270-273).
 #pragma once
+#include <type_traits>
 #include "aqif_warp.cuh"
 
 namespace paqif {
@@ -18,7 +19,10 @@ constexpr int kZPrefetch = 4;  // record chunks prefetched into L2 ahead of the 
 
 template <int BETA>
 struct ZChunk {
-  static constexpr int ZC = BETA * ((8 + BETA - 1) / BETA);  // levels per chunk, multiple of BETA
+#ifndef PAQIF_ZCHUNK
+#define PAQIF_ZCHUNK 8
+#endif
+  static constexpr int ZC = BETA * ((PAQIF_ZCHUNK + BETA - 1) / BETA);  // levels per chunk, multiple of BETA
   static constexpr int kRing = 2 * ZC * PivotLayout<BETA>::kSize;  // doubles
 };
 
@@ -193,6 +197,30 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
     cp_async_commit();
   };
   int status = 0;
+  auto chunk = [&](const double* buf, int k_lo, int c0, auto LAST) {
+#pragma unroll
+    for (int ph = 0; ph < ZC; ++ph) {
+      const int p = p0 + c0 + ph;
+      if (decltype(LAST)::value && p >= s) break;
+      const double* rec = buf + (s - p - k_lo) * RS;
+      double xp, xq;
+      bool ok;
+      if constexpr (EXACT)
+        ok = (FULL && p < BETA)
+                 ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
+                 : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
+      else
+        ok = (FULL && p < BETA) ? zlevel_fma2<BETA, true>(rec, p, n, xp, xq, xl, xr, ph)
+                                : zlevel_fma2<BETA, false>(rec, p, n, xp, xq, xl, xr, ph);
+      if (SCAN)
+        status = ok ? status : s - p;  // ascending p: the last one is the smallest level
+      else
+        status = (!ok & (status == 0)) ? p + 1 : status;  // first failing level, no branch
+      x[sd == 0 ? p : n - 1 - p] = sd == 0 ? xp : xq;
+      xl[ph % BETA] = xp;
+      xr[ph % BETA] = xq;
+    }
+  };
   if (M > 0) issue(0, 0);
   for (int c0 = 0, cb = 0; c0 < M; c0 += ZC, cb ^= 1) {
     if (c0 + ZC < M) {
@@ -206,28 +234,11 @@ __device__ int zsolve_group(const double* zs, int n, double* x, double* ring, in
       const int k_hi = s - p0 - c0;
       const int k_lo = max(1, k_hi - ZC + 1);
       const double* buf = ring + cb * ZC * RS;
-#pragma unroll
-      for (int ph = 0; ph < ZC; ++ph) {
-        const int p = p0 + c0 + ph;
-        if (p >= s) break;
-        const double* rec = buf + (s - p - k_lo) * RS;
-        double xp, xq;
-        bool ok;
-        if constexpr (EXACT)
-          ok = (FULL && p < BETA)
-                   ? zlevel<BETA, EXACT, true>(rec, sd, p, n, xp, xq, xl, xr, ph, pair)
-                   : zlevel<BETA, EXACT, false>(rec, sd, p, n, xp, xq, xl, xr, ph, pair);
-        else
-          ok = (FULL && p < BETA) ? zlevel_fma2<BETA, true>(rec, p, n, xp, xq, xl, xr, ph)
-                                  : zlevel_fma2<BETA, false>(rec, p, n, xp, xq, xl, xr, ph);
-        if (SCAN)
-          status = ok ? status : s - p;  // ascending p: the last one is the smallest level
-        else
-          status = (!ok & (status == 0)) ? p + 1 : status;  // first failing level, no branch
-        x[sd == 0 ? p : n - 1 - p] = sd == 0 ? xp : xq;
-        xl[ph % BETA] = xp;
-        xr[ph % BETA] = xq;
-      }
+      // a full chunk runs its ZC levels as one straight-line block (no
+      // per-level exit test, so the next level's loads and older terms
+      // interleave with this level's chain); the last chunk checks
+      if (c0 + ZC <= M) chunk(buf, k_lo, c0, std::false_type{});
+      else chunk(buf, k_lo, c0, std::true_type{});
     }
     if (!SCAN) {
       // group-uniform status (lane 0 of the group holds it)
