@@ -209,3 +209,26 @@ def test_lcp_wild_systems_fma_status(beta):
     assert np.array_equal(r.active[ok], act[ok])
     scale = np.maximum(1.0, np.max(np.abs(u[ok]), axis=1, keepdims=True))
     assert np.max(np.abs(r.u[ok] - u[ok]) / scale) <= 1e-9
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_lcp_breakdown_levels_both_arithmetics(exact):
+    """Breakdown levels in every range the level test covers: an inner level
+    (found by the Z solve's scan in FMA arithmetic), an outer corner level
+    (found by the corner system), and level 1 -- the same level in both
+    arithmetics, reported as -(level) in res."""
+    from paper_2008_03276_b200.batch import lcp_batch
+    n, beta = 64, 4
+    s = n // 2
+    bands = np.zeros((3, 2 * beta + 1, n))
+    bands[:, beta, :] = 2.0
+    f = np.ones((3, n))
+    # system 0: row 2 singular -> the level-30 pivot (rows 2, 61): a corner level
+    bands[0, beta, 2] = 0.0
+    # system 1: row 20 singular -> level 12 (rows 20, 43): an inner level
+    bands[1, beta, 20] = 0.0
+    # system 2: the middle rows singular -> level 1
+    bands[2, beta, s - 1] = 0.0
+    r = lcp_batch(bands, f, exact=exact)
+    assert list(r.status) == [1, 1, 1]
+    assert list(r.res) == [-float(s - 2), -float(s - 20), -1.0]
