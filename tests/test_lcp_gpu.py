@@ -232,3 +232,26 @@ def test_lcp_breakdown_levels_both_arithmetics(exact):
     r = lcp_batch(bands, f, exact=exact)
     assert list(r.status) == [1, 1, 1]
     assert list(r.res) == [-float(s - 2), -float(s - 20), -1.0]
+
+
+@pytest.mark.parametrize("beta", [1, 2, 5, 8])
+@pytest.mark.parametrize("exact", [True, False])
+def test_lcp_minimum_order_and_odd_batches(beta, exact):
+    """The smallest order the block method allows (n = 2*beta + 2: every
+    hook past the matrix, one middles level) and batches that leave a
+    system group of the last warp empty, both arithmetics, against the
+    oracle (bit-exact / within 1e-9)."""
+    from paper_2008_03276_b200.batch import lcp_batch
+    from paper_2008_03276_b200.workloads import lcp_batch as gen
+    for n, B in ((2 * beta + 2, 3), (2 * beta + 4, 1), (4 * beta + 2, 5)):
+        bands, f = gen(31 + n, B, n=n, beta=beta)
+        u, act, passes, res, st = O.lcp_batch(bands, f, threads=4)
+        r = lcp_batch(bands, f, exact=exact)
+        assert np.array_equal(r.status, st)
+        assert np.array_equal(r.passes, passes)
+        assert np.array_equal(r.active, act)
+        if exact:
+            assert np.array_equal(_bits(r.u), _bits(u))
+        else:
+            scale = np.maximum(1.0, np.max(np.abs(u), axis=1, keepdims=True))
+            assert np.max(np.abs(r.u - u) / scale) <= 1e-9
