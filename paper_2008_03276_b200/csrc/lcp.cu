@@ -108,7 +108,7 @@ struct LcpSmem {
   using PL = PivotLayout<BETA>;
   static constexpr int ZC = ZChunk<BETA>::ZC;
   static constexpr int kM = 2 * BETA;
-  static constexpr int kCorner = 2 * kM * kM + 2 * kM;
+  static constexpr int kCorner = 2 * kM * kM + 3 * kM;
   static constexpr int kRing = 2 * ZC * PL::kSize;
   static constexpr int kScratch = kRing > kCorner ? kRing : kCorner;
   // the factorization's prefetch slots and the Z-solve ring / corner system
@@ -143,6 +143,7 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
   double* rtr = rd + m * m;
   double* fd = rtr + m * m;
   double* rtf = fd + m;
+  double* rinv = rtf + m;  // FMA arithmetic: 1 / diag of the Cholesky factor
   {
     int lv = 0;
     if (alive && gl < BETA - 1) {
@@ -215,12 +216,18 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
     }
     __syncwarp();
     if (alive && !fail) {
+      // reference rounding divides every entry; FMA arithmetic multiplies by
+      // one reciprocal per column (kept for the substitutions)
+      const double inv = EXACT ? 0.0 : 1.0 / ajj;
       for (int k = j + 1 + gl; k < m; k += G) {
         double v = rtr[j * m + k];
         for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtr[i * m + k]));
-        rtr[j * m + k] = A::div(v, ajj);
+        rtr[j * m + k] = EXACT ? A::div(v, ajj) : v * inv;
       }
-      if (gl == 0) rtr[j * m + j] = ajj;
+      if (gl == 0) {
+        rtr[j * m + j] = ajj;
+        if (!EXACT) rinv[j] = inv;
+      }
     }
     __syncwarp();
   }
@@ -228,12 +235,12 @@ __device__ int corner_solve(const double* zs, int n, double* x, double* cs, int 
     for (int j = 0; j < m; ++j) {
       double v = rtf[j];
       for (int i = 0; i < j; ++i) v = A::sub(v, A::mul(rtr[i * m + j], rtf[i]));
-      rtf[j] = A::div(v, rtr[j * m + j]);
+      rtf[j] = EXACT ? A::div(v, rtr[j * m + j]) : v * rinv[j];
     }
     for (int j = m - 1; j >= 0; --j) {
       double v = rtf[j];
       for (int k = j + 1; k < m; ++k) v = A::sub(v, A::mul(rtr[j * m + k], rtf[k]));
-      rtf[j] = A::div(v, rtr[j * m + j]);
+      rtf[j] = EXACT ? A::div(v, rtr[j * m + j]) : v * rinv[j];
     }
     for (int i = 0; i < BETA; ++i) {
       x[i] = rtf[i];
