@@ -119,6 +119,9 @@ __device__ __forceinline__ bool zlevel_fma2(const double* rec, int p, int n, dou
   // branch-free: a det outside the normal range fails the test above
   const double y = rcp_nobranch(det);
   const double2 yy = r2[PL::kYT / 2];
+  // both partial sums run oldest unknown first (left: x[p-BETA] .. x[p-2];
+  // right: x[q+BETA] .. x[q+2]), so only their last terms wait for the pair
+  // solved two levels ago (the pair of the previous level enters after)
   double acc_t = yy.x, acc_b = yy.y, accr_t = 0.0, accr_b = 0.0;
 #pragma unroll
   for (int t = 0; t < BETA; ++t) {
@@ -128,9 +131,10 @@ __device__ __forceinline__ bool zlevel_fma2(const double* rec, int p, int n, dou
       acc_t = A::axpy_neg(acc_t, z.x, xv);
       acc_b = A::axpy_neg(acc_b, z.y, xv);
     }
-    if (t != 0 && (!CHECK || q + 1 + t < n)) {
-      const double2 z = r2[PL::zi(1, 1 + t, 0) / 2];
-      const double xv = xr[(ph - 1 - t + 2 * BETA) % BETA];
+    const int tr = BETA - 1 - t;  // BETA-1 .. 0 (term tr = 0 is the newest: last, below)
+    if (tr != 0 && (!CHECK || q + 1 + tr < n)) {
+      const double2 z = r2[PL::zi(1, 1 + tr, 0) / 2];
+      const double xv = xr[(ph - 1 - tr + 2 * BETA) % BETA];
       accr_t = A::axpy_neg(accr_t, z.x, xv);
       accr_b = A::axpy_neg(accr_b, z.y, xv);
     }
