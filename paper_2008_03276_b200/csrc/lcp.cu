@@ -89,6 +89,9 @@ __device__ __forceinline__ double np_min(double a, double b) {
 }
 
 constexpr int kLcpWarpsPerBlock = 4;
+#ifndef PAQIF_CHECK_PF
+#define PAQIF_CHECK_PF 2  // complementarity-check steps the L1 prefetch runs ahead
+#endif
 #ifndef PAQIF_LCP_MINB
 #define PAQIF_LCP_MINB 2  // resident blocks per SM the register budget is sized for
 #endif
@@ -458,7 +461,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         int i = gl;
         for (; i < BETA; i += G) edge_row(i);  // G >= BETA: at most one
         for (; i + G < n - BETA; i += 2 * G) {
-          prefetch_rows(i - gl + 4 * G);
+          prefetch_rows(i - gl + 2 * PAQIF_CHECK_PF * G);
           double av0[ND], xv0[ND], av1[ND], xv1[ND];
 #pragma unroll
           for (int d = 0; d < ND; ++d) {
