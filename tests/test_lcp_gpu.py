@@ -255,3 +255,19 @@ def test_lcp_minimum_order_and_odd_batches(beta, exact):
         else:
             scale = np.maximum(1.0, np.max(np.abs(u), axis=1, keepdims=True))
             assert np.max(np.abs(r.u - u) / scale) <= 1e-9
+
+
+def test_lcp_fma_matches_reference_goldens():
+    """The headline arithmetic against the reference's own answers: same
+    pass count and cavitated set, values within 1e-9 relative."""
+    from paper_2008_03276_b200.batch import lcp_batch
+    for G in golden_cases("lcp.npz"):
+        if (G["bands"].shape[0] - 1) // 2 > 8:
+            continue
+        r = lcp_batch(G["bands"][None], G["f"][None], exact=False)
+        ref = G["u"]
+        assert r.status[0] == 0
+        assert r.passes[0] == int(G["passes"])
+        scale = max(1.0, float(np.max(np.abs(ref))))
+        assert np.max(np.abs(r.u[0] - ref)) <= 1e-9 * scale
+        assert np.array_equal(cavitated(r.u[0]), cavitated(ref))
