@@ -758,7 +758,10 @@ extern "C" int paqif_solve_r1_batch(int64_t B, int64_t n, int64_t beta, const do
 namespace {
 // Device staging reused across host-entry calls (grown on demand), so the
 // host path pays for copies and the kernel, not for cudaMalloc each call.
-constexpr int kHostChunksMax = 4;
+#ifndef PAQIF_HOST_CHUNKS
+#define PAQIF_HOST_CHUNKS 4
+#endif
+constexpr int kHostChunksMax = PAQIF_HOST_CHUNKS;
 
 struct HostStage {
   std::mutex mu;
