@@ -72,12 +72,8 @@ struct LcpPol {
       if (idx < NP) dst[idx] = src[idx];
     }
   }
-  // all records in global memory before the corner system / Z solve read
-  // them (the warp barrier orders the lanes' stores); all lanes call
-  __device__ __forceinline__ void records_done(int) { __syncwarp(); }
   __device__ __forceinline__ void on_w(int, int, double, double) {}
   __device__ __forceinline__ void on_resid(int, int, double) {}
-  __device__ __forceinline__ const double* record(int k) const { return zs + (size_t)k * PL::kSize; }
 };
 
 __device__ __forceinline__ double fmax_(double a, double b) { return b > a ? b : a; }
@@ -357,7 +353,7 @@ lcp_kernel(int64_t B, int n, const double* __restrict__ bands, const double* __r
         brk_level = fst;
         active = false;
       }
-      pol.records_done(gl);
+      __syncwarp();  // every record stored before the corner system / Z solve read them
       PAQIF_TSTAMP(t1);
       // the factorization's breakdown test runs on the records: here for
       // the outermost levels, in the Z solve for the rest; a breakdown
